@@ -1,0 +1,151 @@
+/*
+ * fermat_b200.h — C ABI of the B200-native batched Fermat path solver.
+ *
+ * Drop-in boundary for the hot path of the reference package `fermatpath`
+ * (/root/reference/pkg/src/fermatpath). The reference is a pure-Python/numpy
+ * library with no FFI of its own; each entry point below replaces the named
+ * reference function and is what its Python layer (or a ctypes/cgo binding,
+ * see INTEGRATION.md) would call.
+ *
+ * Conventions
+ *   - All array arguments are DEVICE pointers (CUDA global memory) in the
+ *     reference's C-contiguous batch layout (batching.py:20-25):
+ *       basis  (B, K, 3, 2)   anchor (B, K, 3)   start/end (B, 3)
+ *       T      (B, K, 2)      points (B, K, 3)   H (B, 2K, 2K)
+ *     except the *_host entry points, which take HOST pointers and do the
+ *     transfers themselves.
+ *   - Every call is asynchronous on `stream` (a cudaStream_t; NULL = legacy
+ *     default stream) and returns an fp_error code; kernels never raise —
+ *     per-path conditions are reported in a status byte (FP_STATUS_*).
+ *   - Optional outputs may be NULL.
+ *   - No global state besides a launch counter (fp_launch_count).
+ */
+#ifndef FERMAT_B200_H
+#define FERMAT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- return codes ------------------------------------------------------ */
+enum fp_error {
+  FP_OK = 0,
+  FP_ERR_INVALID_ARGUMENT = 1,   /* negative sizes, iterations < 1, NULL required ptr */
+  FP_ERR_UNSUPPORTED_ORDER = 2,  /* K outside [0, FP_MAX_ORDER] */
+  FP_ERR_CUDA = 3,               /* a CUDA runtime call failed (see fp_last_cuda_error) */
+  FP_ERR_UNSUPPORTED_MODE = 4
+};
+
+/* Largest interaction count served by the register-resident kernels. The
+ * reference allows up to 64 (geometry.py:23); orders above this are rejected. */
+#define FP_MAX_ORDER 8
+
+/* ---- per-path status bits (uint8) --------------------------------------- */
+#define FP_STATUS_DEGENERATE_ENTRY 0x01u /* entry segment <= eps: reference raises DegenerateSegment for the batch (solver.py:166) */
+#define FP_STATUS_ZERO_DIRECTION   0x02u /* a line search met a zero direction, alpha kept (solver.py:100,110-111) */
+#define FP_STATUS_NOT_STATIONARY   0x04u /* |g| >= 1e-5 (1 + L) at the returned T (implicit_diff.py:30-36) */
+#define FP_STATUS_NONFINITE        0x08u /* non-finite T, g, L or gradient output */
+#define FP_STATUS_DEGENERATE_FINAL 0x10u /* a segment at T <= eps: objective.py:25-31 would raise */
+#define FP_STATUS_SINGULAR         0x20u /* active Hessian singular even with Tikhonov (implicit_diff.py:64-71) */
+#define FP_STATUS_OUT_OF_BOUNDS    0x40u /* enumeration: an interaction point lies outside its object */
+#define FP_STATUS_SHORT_SEGMENT    0x80u /* min segment < 1e-3 at T (near a kink; parity-excluded) */
+/* A path is "converged" when none of these bits is set. */
+#define FP_STATUS_UNCONVERGED_MASK \
+  (FP_STATUS_DEGENERATE_ENTRY | FP_STATUS_NOT_STATIONARY | FP_STATUS_NONFINITE | FP_STATUS_DEGENERATE_FINAL)
+
+/* ---- VJP modes ---------------------------------------------------------- */
+enum fp_vjp_mode {
+  /* w_L * (dL/dtheta + vjp_solution(grad_T L)) + vjp_solution(v_T):
+   * the chain-rule ("full") total derivative, implicit_diff.py:92-100 */
+  FP_VJP_FULL = 0,
+  /* w_L * dL/dtheta|_T + vjp_solution(v_T): the envelope value returned by
+   * grad_length_wrt_params (implicit_diff.py:80-106) */
+  FP_VJP_ENVELOPE = 1,
+  /* w_L * dL/dtheta|_T + param_vjp(T, v_T): v_T is used directly as the
+   * direction u (objective.length_param_gradient / param_vjp,
+   * objective.py:89-135); no stationarity solve, fp_vjp_* only */
+  FP_VJP_MIXED = 2
+};
+
+/* ---- forward solve: solver._bfgs_kernel (solver.py:146-215) -------------
+ * Fixed-iteration batch BFGS with the paper's fixed-point step size.
+ * T0 (B,K,2) in; T_out/g_out (B,K,2), points_out (B,K,3), length_out (B),
+ * status_out (B), trace_len/trace_gnorm (iterations, B) [record_trace],
+ * H_out (B,2K,2K) [return_state]. */
+int fp_solve_f32(const float* basis, const float* anchor, const float* start, const float* end,
+                 const float* T0, int64_t B, int K, int iterations, int fp_iters,
+                 float* T_out, float* g_out, float* points_out, float* length_out,
+                 uint8_t* status_out, float* trace_len, float* trace_gnorm, float* H_out,
+                 void* stream);
+int fp_solve_f64(const double* basis, const double* anchor, const double* start, const double* end,
+                 const double* T0, int64_t B, int K, int iterations, int fp_iters,
+                 double* T_out, double* g_out, double* points_out, double* length_out,
+                 uint8_t* status_out, double* trace_len, double* trace_gnorm, double* H_out,
+                 void* stream);
+
+/* ---- implicit-gradient VJP: implicit_diff.vjp_solution / grad_length_wrt_params
+ * (implicit_diff.py:39-106 over objective.py:48-135), batched.
+ * Cotangents: v_T (B,K,2) on T* (NULL = 0); w_L (B) per-path weight on L*
+ * (NULL = use w_L_scale for every path). Outputs d_basis (B,K,3,2),
+ * d_anchor (B,K,3), d_start (B,3), d_end (B,3); u_out (B,K,2) is the
+ * solve_stationary_system solution for rhs w_L*g + v_T (FULL) or v_T. */
+int fp_vjp_f32(const float* basis, const float* anchor, const float* start, const float* end,
+               const float* T, const float* v_T, const float* w_L, float w_L_scale, int mode,
+               int64_t B, int K, float* d_basis, float* d_anchor, float* d_start, float* d_end,
+               float* u_out, uint8_t* status_out, void* stream);
+int fp_vjp_f64(const double* basis, const double* anchor, const double* start, const double* end,
+               const double* T, const double* v_T, const double* w_L, double w_L_scale, int mode,
+               int64_t B, int K, double* d_basis, double* d_anchor, double* d_start, double* d_end,
+               double* u_out, uint8_t* status_out, void* stream);
+
+/* ---- fused forward + VJP of w_L * L* (one kernel; the config-2 step) ----- */
+int fp_solve_vjp_f32(const float* basis, const float* anchor, const float* start, const float* end,
+                     const float* T0, int64_t B, int K, int iterations, int fp_iters,
+                     const float* w_L, float w_L_scale, int mode,
+                     float* T_out, float* points_out, float* length_out,
+                     float* d_basis, float* d_anchor, float* d_start, float* d_end,
+                     uint8_t* status_out, void* stream);
+
+/* Same step with HOST buffers: copies in, solves + differentiates, copies
+ * out, pipelined over chunks on `nstreams` internal streams; blocks until the
+ * outputs are in host memory. Pinned host memory gives full PCIe bandwidth. */
+int fp_solve_vjp_host_f32(const float* basis, const float* anchor, const float* start,
+                          const float* end, const float* T0, int64_t B, int K, int iterations,
+                          int fp_iters, float w_L_scale, int mode, float* T_out, float* points_out,
+                          float* length_out, float* d_basis, float* d_anchor, float* d_start,
+                          float* d_end, uint8_t* status_out, int64_t chunk, int nstreams);
+
+/* ---- objective pieces: objective.path_length / gradient / hessian
+ * (objective.py:34-64), unclamped norms; degenerate segments flag
+ * FP_STATUS_DEGENERATE_FINAL instead of raising. hess_out (B,2K,2K). */
+int fp_objective_f64(const double* basis, const double* anchor, const double* start,
+                     const double* end, const double* T, int64_t B, int K, double* length_out,
+                     double* grad_out, double* hess_out, uint8_t* status_out, void* stream);
+
+/* ---- solver.line_search_alpha (solver.py:115-143), batched, fp64.
+ * status: FP_STATUS_ZERO_DIRECTION (ZeroDirection) or
+ * FP_STATUS_DEGENERATE_ENTRY (DegenerateSegment in a denominator). */
+int fp_line_search_f64(const double* basis, const double* anchor, const double* start,
+                       const double* end, const double* T, const double* P, const double* alpha0,
+                       int64_t B, int K, int k, double* alpha_out, uint8_t* status_out,
+                       void* stream);
+
+/* ---- solver.init_params (solver.py:67-81), batched, fp64 ----------------- */
+int fp_init_params_f64(const double* basis, const double* anchor, const double* start,
+                       const double* end, int64_t B, int K, double* T_out, void* stream);
+
+/* ---- bookkeeping ---------------------------------------------------------- */
+/* Number of kernels this library has launched in the process (monotone). */
+uint64_t fp_launch_count(void);
+/* Last CUDA error seen by the library (cudaError_t as int). */
+int fp_last_cuda_error(void);
+const char* fp_error_string(int code);
+int fp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FERMAT_B200_H */

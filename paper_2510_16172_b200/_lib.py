@@ -1,0 +1,118 @@
+"""ctypes binding of the C ABI in include/fermat_b200.h.
+
+The shared library is the product: there is no CPU fallback. If it is
+missing, every entry point raises ExtensionMissing (build it with
+``python -m paper_2510_16172_b200.build``).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+from .errors import FermatPathError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libfermat_b200.so")
+HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                      "include", "fermat_b200.h")
+
+FP_OK = 0
+FP_ERR_INVALID_ARGUMENT = 1
+FP_ERR_UNSUPPORTED_ORDER = 2
+FP_ERR_CUDA = 3
+FP_ERR_UNSUPPORTED_MODE = 4
+FP_MAX_ORDER = 8
+
+STATUS_DEGENERATE_ENTRY = 0x01
+STATUS_ZERO_DIRECTION = 0x02
+STATUS_NOT_STATIONARY = 0x04
+STATUS_NONFINITE = 0x08
+STATUS_DEGENERATE_FINAL = 0x10
+STATUS_SINGULAR = 0x20
+STATUS_OUT_OF_BOUNDS = 0x40
+STATUS_SHORT_SEGMENT = 0x80
+STATUS_UNCONVERGED_MASK = (STATUS_DEGENERATE_ENTRY | STATUS_NOT_STATIONARY
+                           | STATUS_NONFINITE | STATUS_DEGENERATE_FINAL)
+
+VJP_FULL = 0
+VJP_ENVELOPE = 1
+VJP_MIXED = 2
+
+
+class ExtensionMissing(RuntimeError):
+    """The CUDA library is not built (or cannot be loaded)."""
+
+
+class CudaCallError(FermatPathError):
+    """A C-ABI call returned an error code."""
+
+
+_P = C.c_void_p
+_I64 = C.c_int64
+_I = C.c_int
+_F = C.c_float
+_D = C.c_double
+
+_SIGS = {
+    "fp_solve_f32": [_P] * 5 + [_I64, _I, _I, _I] + [_P] * 8 + [_P],
+    "fp_solve_f64": [_P] * 5 + [_I64, _I, _I, _I] + [_P] * 8 + [_P],
+    "fp_vjp_f32": [_P] * 7 + [_F, _I, _I64, _I] + [_P] * 6 + [_P],
+    "fp_vjp_f64": [_P] * 7 + [_D, _I, _I64, _I] + [_P] * 6 + [_P],
+    "fp_solve_vjp_f32": [_P] * 5 + [_I64, _I, _I, _I, _P, _F, _I] + [_P] * 8 + [_P],
+    "fp_solve_vjp_host_f32": [_P] * 5 + [_I64, _I, _I, _I, _F, _I] + [_P] * 8 + [_I64, _I],
+    "fp_objective_f64": [_P] * 5 + [_I64, _I] + [_P] * 4 + [_P],
+    "fp_line_search_f64": [_P] * 7 + [_I64, _I, _I] + [_P] * 2 + [_P],
+    "fp_init_params_f64": [_P] * 4 + [_I64, _I, _P, _P],
+    "fp_launch_count": [],
+    "fp_last_cuda_error": [],
+    "fp_error_string": [_I],
+    "fp_version": [],
+}
+_RESTYPES = {"fp_launch_count": C.c_uint64, "fp_error_string": C.c_char_p}
+
+_lib = None
+
+
+def declared_symbols() -> list[str]:
+    """Function names declared in include/fermat_b200.h."""
+    with open(HEADER) as fh:
+        text = fh.read()
+    return sorted(set(re.findall(r"\b(fp_[a-z0-9_]+)\s*\(", text)))
+
+
+def load():
+    """Load the library (once); raises ExtensionMissing if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ExtensionMissing(
+            f"{LIB_PATH} is not built; run `python -m paper_2510_16172_b200.build` "
+            "(the solver has no CPU fallback)")
+    try:
+        lib = C.CDLL(LIB_PATH)
+    except OSError as exc:  # pragma: no cover - environment specific
+        raise ExtensionMissing(f"cannot load {LIB_PATH}: {exc}") from exc
+    for name, args in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = _RESTYPES.get(name, C.c_int)
+    _lib = lib
+    return lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc == FP_OK:
+        return
+    lib = load()
+    msg = lib.fp_error_string(rc).decode()
+    if rc == FP_ERR_UNSUPPORTED_ORDER:
+        raise NotImplementedError(f"{what}: {msg} (max order {FP_MAX_ORDER})")
+    if rc == FP_ERR_INVALID_ARGUMENT:
+        raise ValueError(f"{what}: {msg}")
+    raise CudaCallError(f"{what}: {msg} (code {rc})")
+
+
+def launch_count() -> int:
+    return int(load().fp_launch_count())

@@ -1,0 +1,113 @@
+"""Build the in-tree CUDA library `paper_2510_16172_b200/lib/libfermat_b200.so`.
+
+Every translation unit is compiled for sm_100a only
+(`-gencode arch=compute_100a,code=sm_100a`, IEEE div/sqrt, `-lineinfo`)
+and linked into one shared library with a plain C ABI
+(include/fermat_b200.h). The per-order kernel units build in parallel.
+
+    python -m paper_2510_16172_b200.build [--force] [-j N]
+"""
+
+from __future__ import annotations
+
+import argparse
+import concurrent.futures as cf
+import hashlib
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+INCLUDE = os.path.join(REPO, "include")
+OUT_DIR = os.path.join(PKG, "lib")
+LIB = os.path.join(OUT_DIR, "libfermat_b200.so")
+OBJ_DIR = os.path.join(REPO, "build", "obj")
+
+ORDERS = range(1, 9)
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = [
+    "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
+    "--expt-relaxed-constexpr", "-I", INCLUDE, "-I", CSRC,
+]
+
+
+def nvcc() -> str:
+    path = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    if not os.path.exists(path):
+        raise RuntimeError("nvcc not found; the CUDA toolkit is required to build")
+    return path
+
+
+def _sources_digest() -> str:
+    h = hashlib.sha256()
+    for root in (CSRC, INCLUDE):
+        for name in sorted(os.listdir(root)):
+            if name.endswith((".cu", ".cuh", ".h")):
+                with open(os.path.join(root, name), "rb") as fh:
+                    h.update(name.encode())
+                    h.update(fh.read())
+    h.update(" ".join(ARCH + NVCC_FLAGS).encode())
+    return h.hexdigest()
+
+
+def _units():
+    units = [(os.path.join(CSRC, "fp_abi.cu"), os.path.join(OBJ_DIR, "fp_abi.o"), [])]
+    for k in ORDERS:
+        units.append((os.path.join(CSRC, "fp_inst.cu"), os.path.join(OBJ_DIR, f"fp_inst_k{k}.o"),
+                      [f"-DFP_INST_K={k}"]))
+    for extra in ("fp_enum.cu", "fp_bucket.cu", "fp_peak.cu"):
+        path = os.path.join(CSRC, extra)
+        if os.path.exists(path):
+            units.append((path, os.path.join(OBJ_DIR, extra.replace(".cu", ".o")), []))
+    return units
+
+
+def _compile(unit):
+    src, obj, defs = unit
+    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *defs, "-c", src, "-o", obj]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {os.path.basename(obj)}:\n{res.stderr}")
+    return obj
+
+
+def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -> str:
+    """Compile and link the library if sources changed; returns its path."""
+    os.makedirs(OUT_DIR, exist_ok=True)
+    os.makedirs(OBJ_DIR, exist_ok=True)
+    stamp = os.path.join(OUT_DIR, ".build_digest")
+    digest = _sources_digest()
+    if not force and os.path.exists(LIB) and os.path.exists(stamp):
+        with open(stamp) as fh:
+            if fh.read().strip() == digest:
+                return LIB
+    units = _units()
+    jobs = jobs or min(len(units), os.cpu_count() or 4)
+    with cf.ThreadPoolExecutor(max_workers=jobs) as ex:
+        objs = list(ex.map(_compile, units))
+    tmp = LIB + ".tmp"
+    cmd = [nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", tmp, *objs, "-lcudart_static"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"link failed:\n{res.stderr}")
+    os.replace(tmp, LIB)
+    with open(stamp, "w") as fh:
+        fh.write(digest)
+    if verbose:
+        print(f"built {LIB}")
+    return LIB
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("-j", type=int, default=None)
+    args = ap.parse_args(argv)
+    build(force=args.force, jobs=args.j, verbose=True)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

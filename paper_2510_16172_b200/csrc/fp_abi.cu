@@ -1,0 +1,533 @@
+// C ABI of the B200 Fermat path solver (include/fermat_b200.h).
+//
+// Validation mirrors the reference's host-side checks (SolveOptions
+// iterations/fixed_point_iters >= 1, solver.py:51-55; interaction count
+// bounds, geometry.py:23); everything per path is reported in status bytes.
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "fp_dispatch.h"
+#include "fp_kernels.cuh"
+
+namespace fp {
+
+static std::atomic<uint64_t> g_launches{0};
+static std::atomic<int> g_last_cuda{0};
+
+void count_launches(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+static int cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return FP_OK;
+  g_last_cuda.store(int(e));
+  return FP_ERR_CUDA;
+}
+
+// ---- K = 0: no interactions (solver.py:160-164); length |end - start| ------
+template <typename R>
+__global__ void order0_kernel(const R* start, const R* end, int64_t B, R* length_out,
+                              const R* wL, R wL_scale, R* d_start, R* d_end, uint8_t* status) {
+  const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  R s[3];
+  R q = R(0);
+  for (int r = 0; r < 3; ++r) {
+    s[r] = end[3 * b + r] - start[3 * b + r];
+    q = fma(s[r], s[r], q);
+  }
+  const R n = Num<R>::sqrt_(q);
+  if (length_out) length_out[b] = n;
+  const R w = wL ? wL[b] : wL_scale;
+  for (int r = 0; r < 3; ++r) {
+    const R u = Num<R>::div(s[r], n);
+    if (d_start) d_start[3 * b + r] = -w * u;
+    if (d_end) d_end[3 * b + r] = w * u;
+  }
+  if (status) status[b] = finite(n) ? 0 : FP_STATUS_NONFINITE;
+}
+
+template <typename R>
+static int run_order0(const R* start, const R* end, int64_t B, R* length_out, const R* wL,
+                      R wL_scale, R* d_start, R* d_end, uint8_t* status, cudaStream_t s) {
+  if (B == 0) return FP_OK;
+  const int t = 256;
+  order0_kernel<R><<<unsigned((B + t - 1) / t), t, 0, s>>>(start, end, B, length_out, wL, wL_scale,
+                                                          d_start, d_end, status);
+  count_launches(1);
+  return cuda_status(cudaGetLastError());
+}
+
+template <typename R>
+static int dispatch(int K, const PathArgs<R>& a, int op, cudaStream_t s) {
+  cudaError_t e;
+  switch (K) {
+    case 1: e = dispatch_k<R, 1>(a, op, 0u, s); break;
+    case 2: e = dispatch_k<R, 2>(a, op, 0u, s); break;
+    case 3: e = dispatch_k<R, 3>(a, op, 0u, s); break;
+    case 4: e = dispatch_k<R, 4>(a, op, 0u, s); break;
+    case 5: e = dispatch_k<R, 5>(a, op, 0u, s); break;
+    case 6: e = dispatch_k<R, 6>(a, op, 0u, s); break;
+    case 7: e = dispatch_k<R, 7>(a, op, 0u, s); break;
+    case 8: e = dispatch_k<R, 8>(a, op, 0u, s); break;
+    default: return FP_ERR_UNSUPPORTED_ORDER;
+  }
+  if ((a.rows ? a.n_rows : a.B) > 0) count_launches(1);
+  return cuda_status(e);
+}
+
+template <typename R>
+static PathArgs<R> blank_args() {
+  PathArgs<R> a;
+  std::memset(&a, 0, sizeof(a));
+  return a;
+}
+
+template <typename R>
+static int solve_impl(const R* basis, const R* anchor, const R* start, const R* end, const R* T0,
+                      int64_t B, int K, int iterations, int fp_iters, R* T_out, R* g_out,
+                      R* points_out, R* length_out, uint8_t* status_out, R* trace_len,
+                      R* trace_gnorm, R* H_out, void* stream) {
+  if (B < 0 || iterations < 1 || fp_iters < 1) return FP_ERR_INVALID_ARGUMENT;
+  if (K < 0 || K > FP_MAX_ORDER) return FP_ERR_UNSUPPORTED_ORDER;
+  if ((trace_len == nullptr) != (trace_gnorm == nullptr)) return FP_ERR_INVALID_ARGUMENT;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (K == 0) {
+    if (B > 0 && (start == nullptr || end == nullptr)) return FP_ERR_INVALID_ARGUMENT;
+    return run_order0<R>(start, end, B, length_out, nullptr, R(0), nullptr, nullptr, status_out, s);
+  }
+  if (B > 0 && (!basis || !anchor || !start || !end || !T0)) return FP_ERR_INVALID_ARGUMENT;
+  PathArgs<R> a = blank_args<R>();
+  a.basis = basis; a.anchor = anchor; a.start = start; a.end = end; a.T = T0;
+  a.B = B; a.iterations = iterations; a.fp_iters = fp_iters;
+  a.T_out = T_out; a.g_out = g_out; a.points_out = points_out; a.length_out = length_out;
+  a.status_out = status_out; a.trace_len = trace_len; a.trace_gnorm = trace_gnorm; a.H_out = H_out;
+  return dispatch<R>(K, a, OP_SOLVE, s);
+}
+
+template <typename R>
+static int vjp_impl(const R* basis, const R* anchor, const R* start, const R* end, const R* T,
+                    const R* v_T, const R* w_L, R w_L_scale, int mode, int64_t B, int K, R* d_basis,
+                    R* d_anchor, R* d_start, R* d_end, R* u_out, uint8_t* status_out, void* stream) {
+  if (B < 0) return FP_ERR_INVALID_ARGUMENT;
+  if (mode != FP_VJP_FULL && mode != FP_VJP_ENVELOPE && mode != FP_VJP_MIXED)
+    return FP_ERR_UNSUPPORTED_MODE;
+  if (K < 0 || K > FP_MAX_ORDER) return FP_ERR_UNSUPPORTED_ORDER;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (K == 0)
+    return run_order0<R>(start, end, B, nullptr, w_L, w_L_scale, d_start, d_end, status_out, s);
+  if (B > 0 && (!basis || !anchor || !start || !end || !T)) return FP_ERR_INVALID_ARGUMENT;
+  PathArgs<R> a = blank_args<R>();
+  a.basis = basis; a.anchor = anchor; a.start = start; a.end = end; a.T = T; a.vT = v_T;
+  a.wL = w_L; a.wL_scale = w_L_scale; a.mode = mode; a.B = B; a.iterations = 1; a.fp_iters = 1;
+  a.d_basis = d_basis; a.d_anchor = d_anchor; a.d_start = d_start; a.d_end = d_end;
+  a.u_out = u_out; a.status_out = status_out;
+  return dispatch<R>(K, a, OP_VJP, s);
+}
+
+template <typename R>
+static int solve_vjp_impl(const R* basis, const R* anchor, const R* start, const R* end,
+                          const R* T0, int64_t B, int K, int iterations, int fp_iters, const R* w_L,
+                          R w_L_scale, int mode, R* T_out, R* points_out, R* length_out, R* d_basis,
+                          R* d_anchor, R* d_start, R* d_end, uint8_t* status_out, cudaStream_t s) {
+  if (B < 0 || iterations < 1 || fp_iters < 1) return FP_ERR_INVALID_ARGUMENT;
+  if (mode != FP_VJP_FULL && mode != FP_VJP_ENVELOPE) return FP_ERR_UNSUPPORTED_MODE;
+  if (K < 0 || K > FP_MAX_ORDER) return FP_ERR_UNSUPPORTED_ORDER;
+  if (K == 0)
+    return run_order0<R>(start, end, B, length_out, w_L, w_L_scale, d_start, d_end, status_out, s);
+  if (B > 0 && (!basis || !anchor || !start || !end || !T0)) return FP_ERR_INVALID_ARGUMENT;
+  PathArgs<R> a = blank_args<R>();
+  a.basis = basis; a.anchor = anchor; a.start = start; a.end = end; a.T = T0;
+  a.wL = w_L; a.wL_scale = w_L_scale; a.mode = mode;
+  a.B = B; a.iterations = iterations; a.fp_iters = fp_iters;
+  a.T_out = T_out; a.points_out = points_out; a.length_out = length_out;
+  a.d_basis = d_basis; a.d_anchor = d_anchor; a.d_start = d_start; a.d_end = d_end;
+  a.status_out = status_out;
+  return dispatch<R>(K, a, OP_SOLVE_VJP, s);
+}
+
+// ---- generic-order helpers (scalar API; any K <= 64) ------------------------
+constexpr int kGenMax = 64;
+
+// objective.path_length / gradient / hessian with unclamped norms.
+template <typename R>
+__global__ void objective_kernel(const R* basis, const R* anchor, const R* start, const R* end,
+                                 const R* T, int64_t B, int K, R* length_out, R* grad_out,
+                                 R* hess_out, uint8_t* status) {
+  const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const R* A = basis + b * 6 * K;
+  R P[kGenMax + 2][3];
+  for (int r = 0; r < 3; ++r) {
+    P[0][r] = start[3 * b + r];
+    P[K + 1][r] = end[3 * b + r];
+  }
+  for (int i = 0; i < K; ++i)
+    for (int r = 0; r < 3; ++r)
+      P[i + 1][r] = fma(A[6 * i + 2 * r + 1], T[b * 2 * K + 2 * i + 1],
+                        A[6 * i + 2 * r] * T[b * 2 * K + 2 * i]) + anchor[b * 3 * K + 3 * i + r];
+  const double dx = double(P[K + 1][0]) - double(P[0][0]), dy = double(P[K + 1][1]) - double(P[0][1]),
+               dz = double(P[K + 1][2]) - double(P[0][2]);
+  const R eps = R(1e-12 * (1.0 + sqrt(dz * dz + (dy * dy + dx * dx))));
+  R u[kGenMax + 1][3], n[kGenMax + 1];
+  R L = R(0);
+  uint8_t st = 0;
+  for (int k = 0; k <= K; ++k) {
+    R q = R(0);
+    for (int r = 0; r < 3; ++r) {
+      u[k][r] = P[k + 1][r] - P[k][r];
+      q = fma(u[k][r], u[k][r], q);
+    }
+    n[k] = Num<R>::sqrt_(q);
+    L += n[k];
+    if (n[k] <= eps) st |= FP_STATUS_DEGENERATE_FINAL;
+    for (int r = 0; r < 3; ++r) u[k][r] = Num<R>::div(u[k][r], n[k]);
+  }
+  if (length_out) length_out[b] = L;
+  if (grad_out)
+    for (int i = 0; i < K; ++i)
+      for (int c = 0; c < 2; ++c) {
+        R acc = R(0);
+        for (int r = 0; r < 3; ++r) acc = fma(A[6 * i + 2 * r + c], u[i][r] - u[i + 1][r], acc);
+        grad_out[b * 2 * K + 2 * i + c] = acc;
+      }
+  if (hess_out) {
+    const int m = 2 * K;
+    R* H = hess_out + b * m * m;
+    for (int e = 0; e < m * m; ++e) H[e] = R(0);
+    // block(i, j) = A_i^T M_k A_j with M_k = (I - u_k u_k^T) / n_k
+    auto amb = [&](int i, int j, int k, int ci, int cj) {
+      R au_i = R(0), au_j = R(0), aa = R(0);
+      for (int r = 0; r < 3; ++r) {
+        au_i = fma(A[6 * i + 2 * r + ci], u[k][r], au_i);
+        au_j = fma(A[6 * j + 2 * r + cj], u[k][r], au_j);
+        aa = fma(A[6 * i + 2 * r + ci], A[6 * j + 2 * r + cj], aa);
+      }
+      return Num<R>::div(aa - au_i * au_j, n[k]);
+    };
+    for (int i = 0; i < K; ++i)
+      for (int ci = 0; ci < 2; ++ci)
+        for (int cj = 0; cj < 2; ++cj) {
+          H[(2 * i + ci) * m + 2 * i + cj] = amb(i, i, i, ci, cj) + amb(i, i, i + 1, ci, cj);
+          if (i + 1 < K) {
+            const R off = -amb(i, i + 1, i + 1, ci, cj);
+            H[(2 * i + ci) * m + 2 * (i + 1) + cj] = off;
+            H[(2 * (i + 1) + cj) * m + 2 * i + ci] = off;
+          }
+        }
+  }
+  if (status) status[b] = st | (finite(L) ? 0 : FP_STATUS_NONFINITE);
+}
+
+// solver.line_search_alpha with caller alpha0 and k iterations (unclamped
+// denominators: a collapsed one reports FP_STATUS_DEGENERATE_ENTRY).
+template <typename R>
+__global__ void line_search_kernel(const R* basis, const R* anchor, const R* start, const R* end,
+                                   const R* T, const R* Pd, const R* alpha0, int64_t B, int K,
+                                   int k_iters, R* alpha_out, uint8_t* status) {
+  const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const R* A = basis + b * 6 * K;
+  R X[kGenMax + 2][3], Wd[kGenMax + 2][3];
+  for (int r = 0; r < 3; ++r) {
+    X[0][r] = start[3 * b + r];
+    X[K + 1][r] = end[3 * b + r];
+    Wd[0][r] = Wd[K + 1][r] = R(0);
+  }
+  for (int i = 0; i < K; ++i)
+    for (int r = 0; r < 3; ++r) {
+      const R* t = T + b * 2 * K + 2 * i;
+      const R* p = Pd + b * 2 * K + 2 * i;
+      X[i + 1][r] = fma(A[6 * i + 2 * r + 1], t[1], A[6 * i + 2 * r] * t[0]) + anchor[b * 3 * K + 3 * i + r];
+      Wd[i + 1][r] = fma(A[6 * i + 2 * r + 1], p[1], A[6 * i + 2 * r] * p[0]);
+    }
+  const double dx = double(X[K + 1][0]) - double(X[0][0]), dy = double(X[K + 1][1]) - double(X[0][1]),
+               dz = double(X[K + 1][2]) - double(X[0][2]);
+  const R eps = R(1e-12 * (1.0 + sqrt(dz * dz + (dy * dy + dx * dx))));
+  uint8_t st = 0;
+  R total = R(0);
+  for (int k = 0; k <= K; ++k) {
+    R q = R(0), a2 = R(0);
+    for (int r = 0; r < 3; ++r) {
+      const R s = X[k + 1][r] - X[k][r];
+      const R d = Wd[k + 1][r] - Wd[k][r];
+      q = fma(s, s, q);
+      a2 = fma(d, d, a2);
+    }
+    if (Num<R>::sqrt_(q) <= eps) st |= FP_STATUS_DEGENERATE_ENTRY;
+    total += a2;
+  }
+  R alpha = alpha0 ? alpha0[b] : R(0);
+  if (total <= Num<R>::tiny()) {
+    st |= FP_STATUS_ZERO_DIRECTION;
+  } else if (!(st & FP_STATUS_DEGENERATE_ENTRY)) {
+    for (int it = 0; it < k_iters; ++it) {
+      R num = R(0), den = R(0);
+      for (int k = 0; k <= K; ++k) {
+        R c = R(0), a2 = R(0), q = R(0);
+        for (int r = 0; r < 3; ++r) {
+          const R s = X[k + 1][r] - X[k][r];
+          const R d = Wd[k + 1][r] - Wd[k][r];
+          const R e = fma(alpha, d, s);
+          c = fma(d, s, c);
+          a2 = fma(d, d, a2);
+          q = fma(e, e, q);
+        }
+        const R n = Num<R>::sqrt_(q);
+        if (n <= eps) st |= FP_STATUS_DEGENERATE_ENTRY;
+        num += Num<R>::div(c, n);
+        den += Num<R>::div(a2, n);
+      }
+      if (st & FP_STATUS_DEGENERATE_ENTRY) break;
+      alpha = -Num<R>::div(num, den);
+    }
+  }
+  alpha_out[b] = alpha;
+  if (status) status[b] = st;
+}
+
+// solver.init_params: least-squares projection of the start/end midpoint onto
+// each surface's active span (2x2 or 1x1 normal equations).
+template <typename R>
+__global__ void init_params_kernel(const R* basis, const R* anchor, const R* start, const R* end,
+                                   int64_t B, int K, R* T_out) {
+  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= B * K) return;
+  const int64_t b = idx / K;
+  const int i = int(idx % K);
+  const R* A = basis + b * 6 * K + 6 * i;
+  R mid[3], c0[3], c1[3];
+  for (int r = 0; r < 3; ++r) {
+    mid[r] = R(0.5) * (start[3 * b + r] + end[3 * b + r]) - anchor[b * 3 * K + 3 * i + r];
+    c0[r] = A[2 * r];
+    c1[r] = A[2 * r + 1];
+  }
+  const bool a0 = c0[0] != R(0) || c0[1] != R(0) || c0[2] != R(0);
+  const bool a1 = c1[0] != R(0) || c1[1] != R(0) || c1[2] != R(0);
+  R g00 = 0, g01 = 0, g11 = 0, r0 = 0, r1 = 0;
+  for (int r = 0; r < 3; ++r) {
+    g00 = fma(c0[r], c0[r], g00);
+    g01 = fma(c0[r], c1[r], g01);
+    g11 = fma(c1[r], c1[r], g11);
+    r0 = fma(c0[r], mid[r], r0);
+    r1 = fma(c1[r], mid[r], r1);
+  }
+  R t0 = R(0), t1 = R(0);
+  if (a0 && a1) {
+    const R det = g00 * g11 - g01 * g01;
+    t0 = Num<R>::div(g11 * r0 - g01 * r1, det);
+    t1 = Num<R>::div(g00 * r1 - g01 * r0, det);
+  } else if (a0) {
+    t0 = Num<R>::div(r0, g00);
+  } else if (a1) {
+    t1 = Num<R>::div(r1, g11);
+  }
+  T_out[b * 2 * K + 2 * i] = t0;
+  T_out[b * 2 * K + 2 * i + 1] = t1;
+}
+
+// ---- host-buffer pipeline for the fused step ---------------------------------
+struct HostPipe {
+  std::mutex mu;
+  std::vector<cudaStream_t> streams;
+  std::vector<void*> bufs;
+  size_t buf_bytes = 0;
+  int device = -1;
+};
+static HostPipe g_pipe;
+
+}  // namespace fp
+
+using namespace fp;
+
+extern "C" {
+
+int fp_solve_f32(const float* basis, const float* anchor, const float* start, const float* end,
+                 const float* T0, int64_t B, int K, int iterations, int fp_iters, float* T_out,
+                 float* g_out, float* points_out, float* length_out, uint8_t* status_out,
+                 float* trace_len, float* trace_gnorm, float* H_out, void* stream) {
+  return solve_impl<float>(basis, anchor, start, end, T0, B, K, iterations, fp_iters, T_out, g_out,
+                           points_out, length_out, status_out, trace_len, trace_gnorm, H_out, stream);
+}
+
+int fp_solve_f64(const double* basis, const double* anchor, const double* start, const double* end,
+                 const double* T0, int64_t B, int K, int iterations, int fp_iters, double* T_out,
+                 double* g_out, double* points_out, double* length_out, uint8_t* status_out,
+                 double* trace_len, double* trace_gnorm, double* H_out, void* stream) {
+  return solve_impl<double>(basis, anchor, start, end, T0, B, K, iterations, fp_iters, T_out, g_out,
+                            points_out, length_out, status_out, trace_len, trace_gnorm, H_out, stream);
+}
+
+int fp_vjp_f32(const float* basis, const float* anchor, const float* start, const float* end,
+               const float* T, const float* v_T, const float* w_L, float w_L_scale, int mode,
+               int64_t B, int K, float* d_basis, float* d_anchor, float* d_start, float* d_end,
+               float* u_out, uint8_t* status_out, void* stream) {
+  return vjp_impl<float>(basis, anchor, start, end, T, v_T, w_L, w_L_scale, mode, B, K, d_basis,
+                         d_anchor, d_start, d_end, u_out, status_out, stream);
+}
+
+int fp_vjp_f64(const double* basis, const double* anchor, const double* start, const double* end,
+               const double* T, const double* v_T, const double* w_L, double w_L_scale, int mode,
+               int64_t B, int K, double* d_basis, double* d_anchor, double* d_start, double* d_end,
+               double* u_out, uint8_t* status_out, void* stream) {
+  return vjp_impl<double>(basis, anchor, start, end, T, v_T, w_L, w_L_scale, mode, B, K, d_basis,
+                          d_anchor, d_start, d_end, u_out, status_out, stream);
+}
+
+int fp_solve_vjp_f32(const float* basis, const float* anchor, const float* start, const float* end,
+                     const float* T0, int64_t B, int K, int iterations, int fp_iters,
+                     const float* w_L, float w_L_scale, int mode, float* T_out, float* points_out,
+                     float* length_out, float* d_basis, float* d_anchor, float* d_start,
+                     float* d_end, uint8_t* status_out, void* stream) {
+  return solve_vjp_impl<float>(basis, anchor, start, end, T0, B, K, iterations, fp_iters, w_L,
+                               w_L_scale, mode, T_out, points_out, length_out, d_basis, d_anchor,
+                               d_start, d_end, status_out, static_cast<cudaStream_t>(stream));
+}
+
+int fp_solve_vjp_host_f32(const float* basis, const float* anchor, const float* start,
+                          const float* end, const float* T0, int64_t B, int K, int iterations,
+                          int fp_iters, float w_L_scale, int mode, float* T_out, float* points_out,
+                          float* length_out, float* d_basis, float* d_anchor, float* d_start,
+                          float* d_end, uint8_t* status_out, int64_t chunk, int nstreams) {
+  if (B < 0 || iterations < 1 || fp_iters < 1 || nstreams < 1 || nstreams > 8)
+    return FP_ERR_INVALID_ARGUMENT;
+  if (K < 0 || K > FP_MAX_ORDER) return FP_ERR_UNSUPPORTED_ORDER;
+  if (B == 0) return FP_OK;
+  if (chunk <= 0) chunk = 1 << 18;
+  chunk = (chunk + kThreads - 1) / kThreads * kThreads;
+  std::lock_guard<std::mutex> lock(g_pipe.mu);
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_status(e);
+  // Per-stream slot: inputs then outputs for `chunk` paths, 256-byte aligned pieces.
+  const int64_t w_in[5] = {6 * K, 3 * K, 3, 3, 2 * K};
+  const int64_t w_out[7] = {2 * K, 3 * K, 1, 6 * K, 3 * K, 3, 3};
+  auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+  size_t slot = al(size_t(chunk));  // status
+  for (int i = 0; i < 5; ++i) slot += al(size_t(chunk * w_in[i]) * sizeof(float));
+  for (int i = 0; i < 7; ++i) slot += al(size_t(chunk * w_out[i]) * sizeof(float));
+  if (g_pipe.device != dev || int(g_pipe.streams.size()) < nstreams || g_pipe.buf_bytes < slot) {
+    for (void* p : g_pipe.bufs) cudaFree(p);
+    for (cudaStream_t s : g_pipe.streams) cudaStreamDestroy(s);
+    g_pipe.bufs.clear();
+    g_pipe.streams.clear();
+    for (int i = 0; i < nstreams; ++i) {
+      cudaStream_t s;
+      if ((e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)) != cudaSuccess) return cuda_status(e);
+      g_pipe.streams.push_back(s);
+      void* p = nullptr;
+      if ((e = cudaMalloc(&p, slot)) != cudaSuccess) return cuda_status(e);
+      g_pipe.bufs.push_back(p);
+    }
+    g_pipe.buf_bytes = slot;
+    g_pipe.device = dev;
+  }
+  const float* hin[5] = {basis, anchor, start, end, T0};
+  float* hout[7] = {T_out, points_out, length_out, d_basis, d_anchor, d_start, d_end};
+  int64_t c = 0;
+  for (int64_t lo = 0; lo < B; lo += chunk, ++c) {
+    const int64_t n = (B - lo < chunk) ? (B - lo) : chunk;
+    const int si = int(c % nstreams);
+    cudaStream_t s = g_pipe.streams[si];
+    char* p = static_cast<char*>(g_pipe.bufs[si]);
+    float* din[5];
+    float* dout[7];
+    for (int i = 0; i < 5; ++i) {
+      din[i] = reinterpret_cast<float*>(p);
+      p += al(size_t(chunk * w_in[i]) * sizeof(float));
+    }
+    for (int i = 0; i < 7; ++i) {
+      dout[i] = reinterpret_cast<float*>(p);
+      p += al(size_t(chunk * w_out[i]) * sizeof(float));
+    }
+    uint8_t* dst = reinterpret_cast<uint8_t*>(p);
+    for (int i = 0; i < 5; ++i) {
+      if (w_in[i] == 0 || hin[i] == nullptr) continue;
+      e = cudaMemcpyAsync(din[i], hin[i] + lo * w_in[i], size_t(n * w_in[i]) * sizeof(float),
+                          cudaMemcpyHostToDevice, s);
+      if (e != cudaSuccess) return cuda_status(e);
+    }
+    int rc = solve_vjp_impl<float>(din[0], din[1], din[2], din[3], din[4], n, K, iterations, fp_iters,
+                                   nullptr, w_L_scale, mode, hout[0] ? dout[0] : nullptr,
+                                   hout[1] ? dout[1] : nullptr, hout[2] ? dout[2] : nullptr,
+                                   hout[3] ? dout[3] : nullptr, hout[4] ? dout[4] : nullptr,
+                                   hout[5] ? dout[5] : nullptr, hout[6] ? dout[6] : nullptr,
+                                   status_out ? dst : nullptr, s);
+    if (rc != FP_OK) return rc;
+    for (int i = 0; i < 7; ++i) {
+      if (w_out[i] == 0 || hout[i] == nullptr) continue;
+      e = cudaMemcpyAsync(hout[i] + lo * w_out[i], dout[i], size_t(n * w_out[i]) * sizeof(float),
+                          cudaMemcpyDeviceToHost, s);
+      if (e != cudaSuccess) return cuda_status(e);
+    }
+    if (status_out) {
+      e = cudaMemcpyAsync(status_out + lo, dst, size_t(n), cudaMemcpyDeviceToHost, s);
+      if (e != cudaSuccess) return cuda_status(e);
+    }
+  }
+  for (int i = 0; i < nstreams; ++i) {
+    e = cudaStreamSynchronize(g_pipe.streams[i]);
+    if (e != cudaSuccess) return cuda_status(e);
+  }
+  return FP_OK;
+}
+
+int fp_objective_f64(const double* basis, const double* anchor, const double* start,
+                     const double* end, const double* T, int64_t B, int K, double* length_out,
+                     double* grad_out, double* hess_out, uint8_t* status_out, void* stream) {
+  if (B < 0) return FP_ERR_INVALID_ARGUMENT;
+  if (K < 0 || K > kGenMax) return FP_ERR_UNSUPPORTED_ORDER;
+  if (B == 0) return FP_OK;
+  const int t = 64;
+  objective_kernel<double><<<unsigned((B + t - 1) / t), t, 0, static_cast<cudaStream_t>(stream)>>>(
+      basis, anchor, start, end, T, B, K, length_out, grad_out, hess_out, status_out);
+  count_launches(1);
+  return cuda_status(cudaGetLastError());
+}
+
+int fp_line_search_f64(const double* basis, const double* anchor, const double* start,
+                       const double* end, const double* T, const double* P, const double* alpha0,
+                       int64_t B, int K, int k, double* alpha_out, uint8_t* status_out,
+                       void* stream) {
+  if (B < 0 || k < 1 || alpha_out == nullptr) return FP_ERR_INVALID_ARGUMENT;
+  if (K < 0 || K > kGenMax) return FP_ERR_UNSUPPORTED_ORDER;
+  if (B == 0) return FP_OK;
+  const int t = 64;
+  line_search_kernel<double><<<unsigned((B + t - 1) / t), t, 0, static_cast<cudaStream_t>(stream)>>>(
+      basis, anchor, start, end, T, P, alpha0, B, K, k, alpha_out, status_out);
+  count_launches(1);
+  return cuda_status(cudaGetLastError());
+}
+
+int fp_init_params_f64(const double* basis, const double* anchor, const double* start,
+                       const double* end, int64_t B, int K, double* T_out, void* stream) {
+  if (B < 0 || T_out == nullptr) return FP_ERR_INVALID_ARGUMENT;
+  if (K < 0 || K > kGenMax) return FP_ERR_UNSUPPORTED_ORDER;
+  if (B == 0 || K == 0) return FP_OK;
+  const int t = 128;
+  const int64_t n = B * K;
+  init_params_kernel<double><<<unsigned((n + t - 1) / t), t, 0, static_cast<cudaStream_t>(stream)>>>(
+      basis, anchor, start, end, B, K, T_out);
+  count_launches(1);
+  return cuda_status(cudaGetLastError());
+}
+
+uint64_t fp_launch_count(void) { return g_launches.load(); }
+int fp_last_cuda_error(void) { return g_last_cuda.load(); }
+
+const char* fp_error_string(int code) {
+  switch (code) {
+    case FP_OK: return "ok";
+    case FP_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case FP_ERR_UNSUPPORTED_ORDER: return "unsupported interaction count";
+    case FP_ERR_CUDA: return cudaGetErrorString(static_cast<cudaError_t>(g_last_cuda.load()));
+    case FP_ERR_UNSUPPORTED_MODE: return "unsupported VJP mode";
+    default: return "unknown error";
+  }
+}
+
+int fp_version(void) { return 1; }
+
+}  // extern "C"

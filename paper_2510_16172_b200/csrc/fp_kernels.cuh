@@ -1,0 +1,416 @@
+// Kernel templates: batched forward solve, fused solve + implicit VJP, and
+// VJP-only, one path per thread.
+//
+// Data movement: each CTA owns kThreads consecutive paths. Their input
+// records are contiguous in the reference layout, so a full CTA stages its
+// slabs (basis, anchor, start, end, T) into shared memory with one TMA bulk
+// copy each (cp.async.bulk + mbarrier complete_tx); partial or unaligned
+// CTAs fall back to coalesced vector loads. Outputs are gathered per slab in
+// shared memory and written back with coalesced stores. With a row index
+// (bucketed dispatch), threads read and write their records directly.
+#pragma once
+
+#include "fp_path.cuh"
+
+namespace fp {
+
+enum Op { OP_SOLVE = 0, OP_SOLVE_VJP = 1, OP_VJP = 2 };
+
+template <typename R>
+struct PathArgs {
+  const R *basis, *anchor, *start, *end;
+  const R* T;       // T0 for the solve, T* for VJP-only
+  const R* vT;      // VJP-only: cotangent on T (B,K,2), may be null
+  const R* wL;      // per-path weight on L, may be null
+  R wL_scale;       // weight used when wL is null
+  int mode;         // fp_vjp_mode
+  int64_t B;        // batch rows (leading dim of every array, incl. traces)
+  int iterations, fp_iters;
+  R *T_out, *g_out, *points_out, *length_out;
+  uint8_t* status_out;
+  R *trace_len, *trace_gnorm, *H_out;
+  R *d_basis, *d_anchor, *d_start, *d_end, *u_out;
+  const int32_t* rows;  // optional row indirection (length n_rows)
+  int64_t n_rows;
+};
+
+// Per-path output destinations (shared-memory slab slots or global records).
+template <typename R>
+struct Outs {
+  R *T, *g, *pts, *len, *db, *da, *d0, *d1, *u;
+  uint8_t* st;
+};
+
+// ---- TMA bulk copy helpers -------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ bool aligned16(const void* p) {
+  return (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
+}
+
+template <typename R>
+__device__ __forceinline__ void coop_copy(R* dst, const R* src, int count) {
+  for (int e = threadIdx.x; e < count; e += blockDim.x) dst[e] = src[e];
+}
+
+// One path's inputs, held in registers.
+template <typename R, int K>
+struct Rec {
+  R b[6 * K], a[3 * K], x0[3], x1[3], T[2 * K], v[2 * K];
+};
+
+template <typename R, int K>
+__device__ __forceinline__ void load_rec(Rec<R, K>& r, const R* b, const R* a, const R* x0,
+                                         const R* x1, const R* T, const R* v) {
+#pragma unroll
+  for (int e = 0; e < 6 * K; ++e) r.b[e] = b[e];
+#pragma unroll
+  for (int e = 0; e < 3 * K; ++e) r.a[e] = a[e];
+#pragma unroll
+  for (int e = 0; e < 3; ++e) {
+    r.x0[e] = x0[e];
+    r.x1[e] = x1[e];
+  }
+#pragma unroll
+  for (int e = 0; e < 2 * K; ++e) {
+    r.T[e] = T[e];
+    r.v[e] = v ? v[e] : R(0);
+  }
+}
+
+// ---- the per-path body -------------------------------------------------------
+template <typename R, int K, unsigned MASK, int OP>
+__device__ __forceinline__ void run_path(const PathArgs<R>& a, int64_t row, const Rec<R, K>& in,
+                                         bool has_v, const Outs<R>& o) {
+  using L = Lay<K, MASK>;
+  constexpr int NA = L::NA;
+  Geo<R, K> G;
+  load_geo<R, K, MASK>(G, in.b, in.a, in.x0, in.x1);
+  PathState<R, K, MASK> P;
+  R tin[K];
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    P.t[L::idx(i, 0)] = in.T[2 * i];
+    if (L::plane(i)) P.t[L::idx(i, 1)] = in.T[2 * i + 1];
+    tin[i] = in.T[2 * i + 1];
+  }
+  uint8_t st = 0;
+  P.eval(G, P.g);
+  if (OP != OP_VJP) {
+    if (P.nmin <= G.eps) st |= FP_STATUS_DEGENERATE_ENTRY;  // checked_segments (solver.py:166)
+    InvHess<R, NA> H;
+    H.identity();
+    for (int it = 0; it < a.iterations; ++it) {
+      R p[NA];
+      H.mul(P.g, p);
+#pragma unroll
+      for (int j = 0; j < NA; ++j) p[j] = -p[j];
+      bool zero;
+      const R alpha = P.step_size(G, p, a.fp_iters, zero);
+      if (zero) st |= FP_STATUS_ZERO_DIRECTION;
+      R sg[NA];
+#pragma unroll
+      for (int j = 0; j < NA; ++j) {
+        sg[j] = alpha * p[j];
+        P.t[j] = P.t[j] + sg[j];
+      }
+      R gn[NA];
+      P.eval(G, gn);
+      R y[NA];
+      R sy = R(0), ss = R(0), yy = R(0);
+#pragma unroll
+      for (int j = 0; j < NA; ++j) {
+        y[j] = gn[j] - P.g[j];
+        sy = fma(sg[j], y[j], sy);
+        ss = fma(sg[j], sg[j], ss);
+        yy = fma(y[j], y[j], yy);
+      }
+      const bool ok = sy > (R(1e-12) * Num<R>::sqrt_(ss)) * Num<R>::sqrt_(yy);
+      if (ok) H.update(sg, y, Num<R>::rcp(sy));
+#pragma unroll
+      for (int j = 0; j < NA; ++j) P.g[j] = gn[j];
+      if (a.trace_len != nullptr) {
+        R q = R(0);
+#pragma unroll
+        for (int j = 0; j < NA; ++j) q = fma(P.g[j], P.g[j], q);
+        a.trace_len[(int64_t)it * a.B + row] = P.len;
+        a.trace_gnorm[(int64_t)it * a.B + row] = Num<R>::sqrt_(q);
+      }
+    }
+    if (a.H_out != nullptr) {
+      R* Ho = a.H_out + row * (4 * K * K);
+#pragma unroll
+      for (int i = 0; i < 2 * K; ++i)
+#pragma unroll
+        for (int j = 0; j < 2 * K; ++j) {
+          const int ii = i >> 1, ci = i & 1, jj = j >> 1, cj = j & 1;
+          const bool ai = ci == 0 || L::plane(ii), aj = cj == 0 || L::plane(jj);
+          R v = (i == j) ? R(1) : R(0);
+          if (ai && aj) v = H.h[InvHess<R, NA>::id(L::idx(ii, ci), L::idx(jj, cj))];
+          Ho[i * 2 * K + j] = v;
+        }
+    }
+  }
+  // Final classification at the returned T.
+  if (!stationary<R, NA>(P.g, P.len)) st |= FP_STATUS_NOT_STATIONARY;
+  if (P.nmin <= G.eps) st |= FP_STATUS_DEGENERATE_FINAL;
+  if (P.nmin < R(1e-3)) st |= FP_STATUS_SHORT_SEGMENT;
+  bool fin = finite(P.len);
+#pragma unroll
+  for (int j = 0; j < NA; ++j) fin = fin && finite(P.t[j]) && finite(P.g[j]);
+
+  R tf[K][2];
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    tf[i][0] = P.t[L::idx(i, 0)];
+    tf[i][1] = L::plane(i) ? P.t[L::idx(i, 1)] : tin[i];
+  }
+  if (OP != OP_VJP) {
+    if (o.T)
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        o.T[2 * i] = tf[i][0];
+        o.T[2 * i + 1] = tf[i][1];
+      }
+    if (o.g)
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        o.g[2 * i] = P.g[L::idx(i, 0)];
+        o.g[2 * i + 1] = L::plane(i) ? P.g[L::idx(i, 1)] : R(0);
+      }
+    if (o.pts) {
+      R X[K + 2][3];
+      P.points(G, X);
+#pragma unroll
+      for (int i = 0; i < K; ++i)
+#pragma unroll
+        for (int r = 0; r < 3; ++r) o.pts[3 * i + r] = X[i + 1][r];
+    }
+    if (o.len) o.len[0] = P.len;
+  }
+  if (OP != OP_SOLVE) {
+    R vf[K][2];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      vf[i][0] = in.v[2 * i];
+      vf[i][1] = in.v[2 * i + 1];
+    }
+    const R wl = a.wL ? a.wL[row] : a.wL_scale;
+    const bool full = a.mode == FP_VJP_FULL;
+    const bool mixed = a.mode == FP_VJP_MIXED;
+    const bool need_solve = !mixed && (has_v || (full && wl != R(0)));
+    SceneGrad<R, K> sg;
+    st |= implicit_vjp<R, K, MASK>(G, P, tf, vf, wl, full, need_solve, mixed, sg);
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        fin = fin && finite(sg.da[i][r]) && finite(sg.db[i][r][0]) && finite(sg.db[i][r][1]);
+        if (o.da) o.da[3 * i + r] = sg.da[i][r];
+        if (o.db) {
+          o.db[6 * i + 2 * r] = sg.db[i][r][0];
+          o.db[6 * i + 2 * r + 1] = sg.db[i][r][1];
+        }
+      }
+      if (o.u) {
+        o.u[2 * i] = sg.u[i][0];
+        o.u[2 * i + 1] = sg.u[i][1];
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      fin = fin && finite(sg.d0[r]) && finite(sg.d1[r]);
+      if (o.d0) o.d0[r] = sg.d0[r];
+      if (o.d1) o.d1[r] = sg.d1[r];
+    }
+  }
+  if (!fin) st |= FP_STATUS_NONFINITE;
+  if (o.st) o.st[0] = st;
+}
+
+// Widths (elements per path) of the staged slabs.
+template <int K>
+struct W {
+  static constexpr int basis = 6 * K, anchor = 3 * K, vec = 3, T = 2 * K, pts = 3 * K;
+  static constexpr int in_elems = basis + anchor + 2 * vec + 2 * T;                   // + vT
+  static constexpr int out_elems = 2 * T + pts + 1 + basis + anchor + 2 * vec + T;  // T g pts len db da d0 d1 u
+  static constexpr int slab_elems = in_elems > out_elems ? in_elems : out_elems;
+};
+
+template <typename R, int K>
+constexpr size_t smem_bytes() {
+  return size_t(W<K>::slab_elems) * kThreads * sizeof(R) + kThreads + 16;
+}
+
+template <typename R, int K, unsigned MASK, int OP>
+__global__ void __launch_bounds__(kThreads) path_kernel(const PathArgs<R> a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bar;
+  using Wk = W<K>;
+  const int tid = threadIdx.x;
+  const int64_t base = int64_t(blockIdx.x) * kThreads;
+  const int64_t total = a.rows ? a.n_rows : a.B;
+  if (base >= total) return;
+  const int n = int(total - base < kThreads ? total - base : int64_t(kThreads));
+
+  if (a.rows != nullptr) {
+    // Bucketed dispatch: direct per-thread records.
+    if (tid >= n) return;
+    const int64_t row = a.rows[base + tid];
+    Outs<R> o;
+    o.T = a.T_out ? a.T_out + row * Wk::T : nullptr;
+    o.g = a.g_out ? a.g_out + row * Wk::T : nullptr;
+    o.pts = a.points_out ? a.points_out + row * Wk::pts : nullptr;
+    o.len = a.length_out ? a.length_out + row : nullptr;
+    o.db = a.d_basis ? a.d_basis + row * Wk::basis : nullptr;
+    o.da = a.d_anchor ? a.d_anchor + row * Wk::anchor : nullptr;
+    o.d0 = a.d_start ? a.d_start + row * 3 : nullptr;
+    o.d1 = a.d_end ? a.d_end + row * 3 : nullptr;
+    o.u = a.u_out ? a.u_out + row * Wk::T : nullptr;
+    o.st = a.status_out ? a.status_out + row : nullptr;
+    Rec<R, K> in;
+    load_rec(in, a.basis + row * Wk::basis, a.anchor + row * Wk::anchor, a.start + row * 3,
+             a.end + row * 3, a.T + row * Wk::T, a.vT ? a.vT + row * Wk::T : nullptr);
+    run_path<R, K, MASK, OP>(a, row, in, a.vT != nullptr, o);
+    return;
+  }
+
+  // ---- stage the CTA's input slabs -----------------------------------------
+  R* sb = reinterpret_cast<R*>(smem);
+  R* sa = sb + kThreads * Wk::basis;
+  R* s0 = sa + kThreads * Wk::anchor;
+  R* s1 = s0 + kThreads * 3;
+  R* sT = s1 + kThreads * 3;
+  R* sv = sT + kThreads * Wk::T;
+  const R* gb = a.basis + base * Wk::basis;
+  const R* ga = a.anchor + base * Wk::anchor;
+  const R* g0 = a.start + base * 3;
+  const R* g1 = a.end + base * 3;
+  const R* gT = a.T + base * Wk::T;
+  const R* gv = a.vT ? a.vT + base * Wk::T : nullptr;
+  const bool tma = n == kThreads && aligned16(gb) && aligned16(ga) && aligned16(g0) &&
+                   aligned16(g1) && aligned16(gT) && (gv == nullptr || aligned16(gv));
+  if (tma) {
+    const uint32_t bb = kThreads * Wk::basis * sizeof(R), ba = kThreads * Wk::anchor * sizeof(R),
+                   bv = kThreads * 3 * sizeof(R), bt = kThreads * Wk::T * sizeof(R);
+    if (tid == 0) mbar_init(&bar, 1);
+    __syncthreads();
+    if (tid == 0) {
+      mbar_expect_tx(&bar, bb + ba + 2 * bv + bt + (gv ? bt : 0));
+      bulk_g2s(sb, gb, bb, &bar);
+      bulk_g2s(sa, ga, ba, &bar);
+      bulk_g2s(s0, g0, bv, &bar);
+      bulk_g2s(s1, g1, bv, &bar);
+      bulk_g2s(sT, gT, bt, &bar);
+      if (gv) bulk_g2s(sv, gv, bt, &bar);
+    }
+    mbar_wait(&bar, 0);
+  } else {
+    coop_copy(sb, gb, n * Wk::basis);
+    coop_copy(sa, ga, n * Wk::anchor);
+    coop_copy(s0, g0, n * 3);
+    coop_copy(s1, g1, n * 3);
+    coop_copy(sT, gT, n * Wk::T);
+    if (gv) coop_copy(sv, gv, n * Wk::T);
+    __syncthreads();
+  }
+
+  // ---- compute (inputs are copied to registers first) ------------------------
+  // Output slabs reuse the same shared memory after the barrier below.
+  R* oT = reinterpret_cast<R*>(smem);
+  R* og = oT + kThreads * Wk::T;
+  R* op = og + kThreads * Wk::T;
+  R* ol = op + kThreads * Wk::pts;
+  R* odb = ol + kThreads;
+  R* oda = odb + kThreads * Wk::basis;
+  R* od0 = oda + kThreads * Wk::anchor;
+  R* od1 = od0 + kThreads * 3;
+  R* ou = od1 + kThreads * 3;
+  uint8_t* ost = reinterpret_cast<uint8_t*>(smem + size_t(Wk::slab_elems) * kThreads * sizeof(R));
+
+  // Copy this thread's inputs out of shared memory into registers, then wait
+  // for every thread before the slab is reused for outputs.
+  Rec<R, K> in;
+  if (tid < n)
+    load_rec(in, sb + tid * Wk::basis, sa + tid * Wk::anchor, s0 + tid * 3, s1 + tid * 3,
+             sT + tid * Wk::T, gv ? sv + tid * Wk::T : nullptr);
+  __syncthreads();
+  if (tid < n) {
+    Outs<R> o;
+    o.T = a.T_out ? oT + tid * Wk::T : nullptr;
+    o.g = a.g_out ? og + tid * Wk::T : nullptr;
+    o.pts = a.points_out ? op + tid * Wk::pts : nullptr;
+    o.len = a.length_out ? ol + tid : nullptr;
+    o.db = a.d_basis ? odb + tid * Wk::basis : nullptr;
+    o.da = a.d_anchor ? oda + tid * Wk::anchor : nullptr;
+    o.d0 = a.d_start ? od0 + tid * 3 : nullptr;
+    o.d1 = a.d_end ? od1 + tid * 3 : nullptr;
+    o.u = a.u_out ? ou + tid * Wk::T : nullptr;
+    o.st = ost + tid;
+    run_path<R, K, MASK, OP>(a, base + tid, in, gv != nullptr, o);
+  }
+  __syncthreads();
+
+  // ---- coalesced write-back ----------------------------------------------------
+  if (a.T_out) coop_copy(a.T_out + base * Wk::T, oT, n * Wk::T);
+  if (a.g_out) coop_copy(a.g_out + base * Wk::T, og, n * Wk::T);
+  if (a.points_out) coop_copy(a.points_out + base * Wk::pts, op, n * Wk::pts);
+  if (a.length_out) coop_copy(a.length_out + base, ol, n);
+  if (a.d_basis) coop_copy(a.d_basis + base * Wk::basis, odb, n * Wk::basis);
+  if (a.d_anchor) coop_copy(a.d_anchor + base * Wk::anchor, oda, n * Wk::anchor);
+  if (a.d_start) coop_copy(a.d_start + base * 3, od0, n * 3);
+  if (a.d_end) coop_copy(a.d_end + base * 3, od1, n * 3);
+  if (a.u_out) coop_copy(a.u_out + base * Wk::T, ou, n * Wk::T);
+  if (a.status_out) coop_copy(a.status_out + base, ost, n);
+}
+
+// Host-side launcher (defined per K in fp_inst.cu).
+template <typename R, int K, unsigned MASK, int OP>
+cudaError_t launch_path(const PathArgs<R>& a, cudaStream_t stream);
+
+template <typename R, int K, unsigned MASK, int OP>
+cudaError_t launch_path_impl(const PathArgs<R>& a, cudaStream_t stream) {
+  const int64_t total = a.rows ? a.n_rows : a.B;
+  if (total <= 0) return cudaSuccess;
+  const size_t smem = smem_bytes<R, K>();
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(path_kernel<R, K, MASK, OP>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const int64_t blocks = (total + kThreads - 1) / kThreads;
+  path_kernel<R, K, MASK, OP><<<dim3(unsigned(blocks)), dim3(kThreads), smem, stream>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace fp

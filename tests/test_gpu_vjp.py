@@ -1,0 +1,140 @@
+"""GPU implicit-gradient parity: the VJP kernel vs the reference's fp64 results."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2510_16172_b200 as fp
+from paper_2510_16172_b200 import _lib, datagen
+from paper_2510_16172_b200.batching import BatchScene
+from paper_2510_16172_b200.implicit_diff import vjp_batch
+from paper_2510_16172_b200.solver import Precision, SolveOptions, solve, solve_with_gradients
+from oracle import fermat_oracle as O
+
+from parity import GRAD_REL, converged_mask, flat_grad, golden, grad_rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def _scene(d, dt):
+    return BatchScene(d["basis"], d["anchor"], d["start"], d["end"]).astype(dt)
+
+
+def _flat(gr):
+    return flat_grad(*(t.double().cpu().numpy() for t in (gr.basis, gr.anchor, gr.start, gr.end)))
+
+
+def _golden_flat(d, prefix):
+    return flat_grad(d[prefix + "_basis"], d[prefix + "_anchor"], d[prefix + "_start"],
+                     d[prefix + "_end"])
+
+
+@pytest.mark.parametrize("K", [1, 2, 3, 4, 5])
+def test_full_gradient_at_reference_solution(K):
+    d = golden(f"fwd_mixed_k{K}")
+    T = d["T_f32"]
+    stat = d["grad_stationary"] & converged_mask(d["basis"], d["anchor"], d["start"], d["end"], T)
+    assert stat.any()
+    ref = _golden_flat(d, "grad_full")
+    # fp32 kernel: the graded path, 1e-3 relative
+    g32, st32, _ = vjp_batch(_scene(d, np.float32), T, w_L=1.0, mode="full")
+    err32 = grad_rel_err(_flat(g32), ref)
+    assert np.all(err32[stat] <= GRAD_REL), err32[stat].max()
+    # fp64 kernel: same formula in double, far tighter
+    g64, st64, _ = vjp_batch(_scene(d, np.float64), T.astype(np.float64), w_L=1.0, mode="full")
+    err64 = grad_rel_err(_flat(g64), ref)
+    assert np.all(err64[stat] <= 1e-9), err64[stat].max()
+    # device stationarity gate (fp64) agrees with the reference's gate
+    dev_stat = (st64.cpu().numpy() & _lib.STATUS_NOT_STATIONARY) == 0
+    assert np.mean(dev_stat == d["grad_stationary"]) >= 0.99
+
+
+@pytest.mark.parametrize("K", [2, 4])
+def test_envelope_and_solution_vjp(K):
+    d = golden(f"fwd_mixed_k{K}")
+    T = d["T_f32"].astype(np.float64)
+    stat = d["grad_stationary"]
+    sc = _scene(d, np.float64)
+    env, _, _ = vjp_batch(sc, T, w_L=1.0, mode="envelope")
+    assert np.all(grad_rel_err(_flat(env), _golden_flat(d, "grad_env"))[stat] <= 1e-12)
+    vj, _, u = vjp_batch(sc, T, v_T=d["grad_v"], mode="envelope", return_u=True)
+    assert np.all(grad_rel_err(_flat(vj), _golden_flat(d, "grad_vjp"))[stat] <= 1e-9)
+    uu = u.cpu().numpy()
+    rel = np.linalg.norm((uu - d["grad_u"]).reshape(len(uu), -1), axis=1) / np.linalg.norm(
+        d["grad_u"].reshape(len(uu), -1), axis=1)
+    assert np.all(rel[stat] <= 1e-9)
+    # fp32 solution VJP within the contract
+    vj32, _, _ = vjp_batch(_scene(d, np.float32), d["T_f32"], v_T=d["grad_v"].astype(np.float32),
+                           mode="envelope")
+    conv = stat & converged_mask(d["basis"], d["anchor"], d["start"], d["end"], d["T_f32"])
+    assert np.all(grad_rel_err(_flat(vj32), _golden_flat(d, "grad_vjp"))[conv] <= GRAD_REL)
+
+
+@pytest.mark.parametrize("kinds", ["reflections", "mixed", "diffractions"])
+def test_scalar_api_at_reference_optimum(kinds):
+    d = golden(f"refgen_{kinds}_n3")
+    from test_gpu_solve import _specs
+    specs = _specs(d)
+    for j, (spec, Tref) in enumerate(zip(specs, d["Tref"])):
+        if not d["grad_stationary"][j]:
+            continue
+        v = d["grad_v"][j]
+        sg = fp.vjp_solution(spec, Tref, v)
+        ref = np.concatenate([d["grad_vjp_basis"][j].ravel(), d["grad_vjp_anchor"][j].ravel(),
+                              d["grad_vjp_start"][j], d["grad_vjp_end"][j]])
+        assert np.linalg.norm(sg.flat() - ref) <= 1e-9 * max(np.linalg.norm(ref), 1e-12)
+        u = fp.solve_stationary_system(spec, Tref, v)
+        assert np.allclose(u, d["grad_u"][j], rtol=1e-9, atol=1e-12)
+        assert np.all(u[~spec.active_mask] == 0.0)
+        env = fp.grad_length_wrt_params(spec, Tref, debug_check=True)
+        ref_env = np.concatenate([d["grad_env_basis"][j].ravel(), d["grad_env_anchor"][j].ravel(),
+                                  d["grad_env_start"][j], d["grad_env_end"][j]])
+        assert np.allclose(env.flat(), ref_env, rtol=1e-12, atol=1e-12)
+        # translation invariance (test_implicit.py:95-101)
+        assert np.allclose(env.start + env.end + env.anchor.sum(axis=0), 0.0, atol=1e-9)
+
+
+def test_not_stationary_raises():
+    d = golden("refgen_mixed_n2")
+    from test_gpu_solve import _specs
+    spec = _specs(d)[0]
+    T = d["Tref"][0] + 0.5 * spec.active_mask
+    with pytest.raises(fp.NotStationary):
+        fp.solve_stationary_system(spec, T, np.ones((2, 2)))
+    with pytest.raises(fp.NotStationary):
+        fp.vjp_solution(spec, T, np.ones((2, 2)))
+
+
+def test_objective_and_mixed_derivatives_match_oracle():
+    d = golden("refgen_mixed_n4")
+    from test_gpu_solve import _specs
+    rng = np.random.default_rng(4)
+    for spec, T0 in list(zip(_specs(d), d["T0"]))[:4]:
+        T = T0 + 0.1 * rng.normal(size=T0.shape) * spec.active_mask
+        args = (spec.basis_tensor, spec.anchor_tensor, spec.start, spec.end, T)
+        assert fp.path_length(spec, T) == pytest.approx(O.scalar_length(*args), rel=1e-14)
+        assert np.allclose(fp.gradient(spec, T), O.scalar_gradient(*args), atol=1e-13)
+        assert np.allclose(fp.hessian(spec, T), O.scalar_hessian(*args), atol=1e-12)
+        pg = fp.length_param_gradient(spec, T)
+        assert np.allclose(pg.flat(), O.flat(O.partial_gradient(*args)), atol=1e-13)
+        U = rng.normal(size=T.shape)
+        mv = fp.param_vjp(spec, T, U)
+        assert np.allclose(mv.flat(), O.flat(O.mixed_vjp(*args, U)), atol=1e-12)
+
+
+def test_fused_step_equals_solve_then_vjp_bitwise():
+    b = datagen.gen_batch(11, datagen.all_orderings(3), 160)
+    sc = BatchScene(b.basis, b.anchor, b.start, b.end)
+    opts = SolveOptions(iterations=20, precision=Precision.SINGLE)
+    res, grads = solve_with_gradients(sc, b.T0, opts, weight=1.0, mode="full")
+    sep = solve(sc, b.T0, opts)
+    g2, st2, _ = vjp_batch(sc, sep.T, w_L=1.0, mode="full")
+    assert torch.equal(res.T, sep.T)
+    assert torch.equal(res.length, sep.length)
+    for a, c in ((grads.basis, g2.basis), (grads.anchor, g2.anchor), (grads.start, g2.start),
+                 (grads.end, g2.end)):
+        assert torch.equal(a, c)
+    w = torch.linspace(0.5, 2.0, b.size, device=res.T.device)
+    _, gw = solve_with_gradients(sc, b.T0, opts, weight=w, mode="full")
+    g3, _, _ = vjp_batch(sc, sep.T, w_L=w, mode="full")
+    assert torch.equal(gw.anchor, g3.anchor)
