@@ -1,0 +1,438 @@
+"""Benchmark: converged Fermat paths/s for the fused forward + implicit-VJP step.
+
+Workload (BASELINE.json config 2 at the headline order K=3): every R/D
+ordering of order 3, 2^22 paths per GPU split evenly over the 8 orderings,
+fp32, zero init, 20 BFGS iterations with one fixed-point step-size
+iteration, then the implicit-differentiation VJP of the summed path length
+w.r.t. TX, RX and every object origin/basis vector. A step is one pass of
+that fused kernel over the batch; inputs (654 MB/step) exceed the 126 MB L2.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Multi-GPU: torchrun, one rank per GPU; each rank owns its own 2^22 paths
+(weak scaling, no data-path collective); time = max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "converged paths/sec (fwd+implicit VJP) at order K"
+UNIT = "paths/s"
+
+
+def flops_per_path(K: int, I: int, F: int = 1) -> tuple[int, int]:
+    """Algorithmic FLOP per path: (forward, VJP).
+
+    add/sub/mul/div/sqrt = 1, FMA = 2; dense uniform 2K formulation.
+    """
+    S = K + 1
+    per_it = 32 * K * K + 90 * K + 29 + (F - 1) * (16 * K + 15)
+    fwd = I * per_it + (25 * K + 12 * S) + (S - 1)
+    vjp = 219 * K + 22 * S - 32
+    return fwd, vjp
+
+
+def bytes_per_path(K: int) -> tuple[int, int]:
+    """HBM bytes per path of the fused step: (read, write)."""
+    read = (6 * K + 3 * K + 3 + 3 + 2 * K) * 4
+    write = (2 * K + 3 * K + 1 + 6 * K + 3 * K + 3 + 3) * 4 + 1
+    return read, write
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML during the timed region."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x2: "applications_clocks_setting", 0x10: "sync_boost"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # pragma: no cover - NVML missing
+            self._nv = None
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self._nv.nvmlDeviceGetClockInfo(self._h, self._nv.NVML_CLOCK_SM))
+                bits = self._nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for b, name in self.REASONS.items():
+                    if bits & b:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._nv is not None:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": float(np.median(self.samples)) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _max_over_ranks(x: float, ws: int, dev) -> float:
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _sum_over_ranks(x: float, ws: int, dev) -> float:
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def _barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def _load_ncu_traffic(K: int):
+    path = os.path.join(REPO, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        ent = d.get(f"fused_k{K}")
+        return None if ent is None else ent.get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+def measure_ffma_peak(lib, stream, dev):
+    """FP32 FFMA peak in TFLOP/s (best of 5, CUDA events)."""
+    import torch
+
+    props = torch.cuda.get_device_properties(dev)
+    blocks = props.multi_processor_count * 8
+    iters = 4096
+    out = torch.zeros(1, device=dev)
+    best = 0.0
+    for _ in range(6):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        rc = lib.fp_peak_ffma(blocks, iters, out.data_ptr(), stream)
+        e1.record()
+        torch.cuda.synchronize()
+        if rc != 0:
+            return None
+        ms = e0.elapsed_time(e1)
+        flops = blocks * 256 * iters * 128 * 2
+        best = max(best, flops / (ms * 1e-3) / 1e12)
+    return best
+
+
+def cpu_sample(batch, n: int):
+    """A bounded, ordering-balanced sample of the workload (every ordering equally)."""
+    K = batch.order
+    nord = max(1, len(batch.orderings))
+    per = max(1, n // nord)
+    rows = np.concatenate([np.arange(lo, lo + min(per, cnt)) for _, lo, cnt in batch.orderings]) \
+        if batch.orderings else np.arange(min(n, batch.size))
+    return (batch.basis[rows], batch.anchor[rows], batch.start[rows], batch.end[rows],
+            batch.T0[rows]), len(rows), K
+
+
+def run_reference(args):
+    """--impl reference: the CPU restatement of the reference path on all host cores."""
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    from paper_2510_16172_b200 import datagen
+    from oracle.cpu_baseline import CpuPool
+
+    K, I = args.order, args.iterations
+    batch = datagen.config2(K, 1 << 12 if args.quick else args.sample)
+    (b, a, s0, s1, T0), n, _ = cpu_sample(batch, batch.size)
+    pool = CpuPool()
+    for _ in range(args.warmup):
+        pool.run(b, a, s0, s1, T0, I)
+    conv_total, wall_total = 0, 0.0
+    for _ in range(args.steps):
+        c, w = pool.run(b, a, s0, s1, T0, I)
+        conv_total += c
+        wall_total += w
+    pool.close()
+    value = conv_total / wall_total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall_total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded numpy PCG64, SURVEY.md §8(d) generator)",
+        "config": _config(K, I, args.paths, ws),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": pool.cores, "kind": "port",
+                         "sample": f"{n} paths per step (all 8 orderings equally) of config 2 K={K}; "
+                                   "oracle/fermat_oracle.py numpy restatement, batched forward + "
+                                   "per-path implicit gradient like the reference"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "converged_fraction": conv_total / (n * args.steps),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _config(K, I, paths, ws):
+    return {"workload": f"config2: every R/D ordering of order K={K}, fwd + full implicit VJP of sum L",
+            "K": K, "orderings": 2 ** K, "paths_per_gpu": paths, "iterations": I, "fp_iters": 1,
+            "init": "zero", "l2": "inputs larger than L2 (no flush needed)",
+            "parallelism": f"dp{ws} (independent path shards)"}
+
+
+def run_ours(args):
+    import torch
+
+    from paper_2510_16172_b200 import _lib, datagen
+    from paper_2510_16172_b200.batching import BatchScene
+
+    ws, rank, local = _dist()
+    if ws > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    lib = _lib.load()
+    K, I, F = args.order, args.iterations, 1
+    B = args.paths
+    host = datagen.gen_batch(100 + K + 1000 * rank, datagen.all_orderings(K), B // 2 ** K)
+    B = host.size
+    sc = BatchScene(host.basis, host.anchor, host.start, host.end)
+    T0 = torch.from_numpy(host.T0).to(dev)
+    f32 = torch.float32
+    outT = torch.empty(B, K, 2, dtype=f32, device=dev)
+    outP = torch.empty(B, K, 3, dtype=f32, device=dev)
+    outL = torch.empty(B, dtype=f32, device=dev)
+    gB = torch.empty(B, K, 3, 2, dtype=f32, device=dev)
+    gA = torch.empty(B, K, 3, dtype=f32, device=dev)
+    g0 = torch.empty(B, 3, dtype=f32, device=dev)
+    g1 = torch.empty(B, 3, dtype=f32, device=dev)
+    st = torch.empty(B, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream().cuda_stream
+    P = lambda t: t.data_ptr()  # noqa: E731
+
+    def step():
+        rc = lib.fp_solve_vjp_f32(P(sc.basis), P(sc.anchor), P(sc.start), P(sc.end), P(T0), B, K,
+                                  I, F, None, 1.0, _lib.VJP_FULL, P(outT), P(outP), P(outL),
+                                  P(gB), P(gA), P(g0), P(g1), P(st), stream)
+        if rc:
+            _lib.check(rc, "fp_solve_vjp_f32")
+
+    def fwd_step():
+        rc = lib.fp_solve_f32(P(sc.basis), P(sc.anchor), P(sc.start), P(sc.end), P(T0), B, K, I, F,
+                              P(outT), None, P(outP), P(outL), P(st), None, None, None, stream)
+        if rc:
+            _lib.check(rc, "fp_solve_f32")
+
+    def timed(fn, steps, warmup, sampler=None):
+        for _ in range(warmup):
+            fn()
+        torch.cuda.synchronize()
+        _barrier(ws)
+        torch.cuda.synchronize()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(steps)]
+        n0 = _lib.launch_count()
+        ctx = sampler if sampler is not None else _Null()
+        with ctx:
+            for e0, e1 in evs:
+                e0.record()
+                fn()
+                e1.record()
+            torch.cuda.synchronize()
+        launches = _lib.launch_count() - n0
+        _barrier(ws)
+        ms = [e0.elapsed_time(e1) for e0, e1 in evs]
+        return float(np.sum(ms)), ms, launches
+
+    # ---- fused forward + VJP step (the headline) ------------------------------
+    sampler = ClockSampler(torch.cuda.current_device())
+    tot_ms, ms_list, launches = timed(step, args.steps, args.warmup, sampler)
+    conv = int(((st & _lib.STATUS_UNCONVERGED_MASK) == 0).sum().item())
+    tot_ms_max = _max_over_ranks(tot_ms, ws, dev)
+    conv_all = _sum_over_ranks(conv, ws, dev)
+    paths_all = _sum_over_ranks(B, ws, dev)
+    step_s = tot_ms_max * 1e-3 / args.steps
+    value = conv_all / step_s
+    raw = paths_all / step_s
+
+    # ---- forward only ------------------------------------------------------------
+    f_ms, f_list, _ = timed(fwd_step, args.steps, args.warmup)
+    f_conv = int(((st & _lib.STATUS_UNCONVERGED_MASK) == 0).sum().item())
+    f_step_s = _max_over_ranks(f_ms, ws, dev) * 1e-3 / args.steps
+    f_conv_all = _sum_over_ranks(f_conv, ws, dev)
+
+    # ---- roofline ------------------------------------------------------------------
+    fl_fwd, fl_vjp = flops_per_path(K, I, F)
+    peak = measure_ffma_peak(lib, stream, dev) if rank == 0 else None
+    avg_launch_s = float(np.mean(ms_list)) * 1e-3
+    achieved = (fl_fwd + fl_vjp) * B / avg_launch_s / 1e12
+    rd, wr = bytes_per_path(K)
+    hbm_gbs = (rd + wr) * B / avg_launch_s / 1e9
+    peaks = {}
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+            peaks = json.load(fh)
+    except (OSError, ValueError):
+        pass
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    traffic = _load_ncu_traffic(K)
+
+    # ---- end to end through the host-buffer C-ABI entry ---------------------------------
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda shape, dt=torch.float32: torch.empty(shape, dtype=dt, pin_memory=True)  # noqa: E731
+        hin = [pin(tuple(host.basis.shape)), pin(tuple(host.anchor.shape)), pin((B, 3)), pin((B, 3)),
+               pin((B, K, 2))]
+        for t, a in zip(hin, (host.basis, host.anchor, host.start, host.end, host.T0)):
+            t.numpy()[...] = a
+        hout = [pin((B, K, 2)), pin((B, K, 3)), pin((B,)), pin((B, K, 3, 2)), pin((B, K, 3)),
+                pin((B, 3)), pin((B, 3)), pin((B,), torch.uint8)]
+        h2d = sum(t.numel() * t.element_size() for t in hin)
+        d2h = sum(t.numel() * t.element_size() for t in hout)
+
+        def e2e_step():
+            rc = lib.fp_solve_vjp_host_f32(*(P(t) for t in hin), B, K, I, F, 1.0, _lib.VJP_FULL,
+                                           *(P(t) for t in hout), args.chunk, 3)
+            if rc:
+                _lib.check(rc, "fp_solve_vjp_host_f32")
+
+        e2e_step()
+        _barrier(ws)
+        e_steps = max(3, args.steps // 4)
+        t0 = time.perf_counter()
+        for _ in range(e_steps):
+            e2e_step()
+        e_s = (time.perf_counter() - t0) / e_steps
+        e_s = _max_over_ranks(e_s, ws, dev)
+        e_conv = int(((hout[7] & _lib.STATUS_UNCONVERGED_MASK) == 0).sum().item())
+        e2e = {"value": _sum_over_ranks(e_conv, ws, dev) / e_s, "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": e_s * 1e3, "raw_paths_per_s": paths_all / e_s,
+               "path": "fp_solve_vjp_host_f32 (pinned host buffers, 3-stream chunked pipeline)"}
+
+    # ---- CPU baseline (rank 0, N=1 only) ----------------------------------------------
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        from oracle.cpu_baseline import CpuPool
+
+        (b, a, s0, s1, T0h), n, _ = cpu_sample(host, 1 << 12 if args.quick else args.sample)
+        pool = CpuPool()
+        pool.run(b[:pool.cores * 8], a[:pool.cores * 8], s0[:pool.cores * 8], s1[:pool.cores * 8],
+                 T0h[:pool.cores * 8], I)  # warm the workers
+        c, w = pool.run(b, a, s0, s1, T0h, I)
+        pool.close()
+        cpu = {"value": c / w, "unit": UNIT, "cores": pool.cores, "kind": "port",
+               "sample": f"{n} paths (all 8 orderings equally) of this workload; numpy "
+                         "restatement (oracle/fermat_oracle.py): batched forward + per-path "
+                         "implicit gradient like the reference", "wall_s": w,
+               "converged_fraction": c / n}
+
+    if rank == 0:
+        clocks = sampler.summary()
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded numpy PCG64, SURVEY.md §8(d) generator)",
+            "config": _config(K, I, B, ws),
+            "raw_paths_per_s": raw, "converged_fraction": conv_all / paths_all,
+            "fwd": {"value": f_conv_all / f_step_s, "raw_paths_per_s": paths_all / f_step_s,
+                    "ms_per_step": f_step_s * 1e3, "unit": UNIT},
+            "roofline": {
+                "bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": (achieved / peak) if peak else None, "traffic": traffic,
+                "flop_per_path": fl_fwd + fl_vjp, "paths_per_launch": B,
+                "peak_source": "FFMA microbenchmark (fp_peak_ffma) measured in this run; "
+                               "MEASURED_PEAKS.json has no FP32 SIMT figure",
+                "hbm": {"achieved": hbm_gbs, "peak": hbm_peak, "unit": "GB/s",
+                        "frac": hbm_gbs / hbm_peak, "bytes_per_path": rd + wr},
+            },
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--order", type=int, default=3)
+    ap.add_argument("--iterations", type=int, default=20)
+    ap.add_argument("--paths", type=int, default=1 << 22, help="paths per GPU")
+    ap.add_argument("--sample", type=int, default=1 << 17, help="CPU baseline sample size")
+    ap.add_argument("--chunk", type=int, default=1 << 19, help="e2e pipeline chunk (paths)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="tiny CPU samples (debugging)")
+    args = ap.parse_args(argv)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -136,6 +136,11 @@ int fp_line_search_f64(const double* basis, const double* anchor, const double* 
 int fp_init_params_f64(const double* basis, const double* anchor, const double* start,
                        const double* end, int64_t B, int K, double* T_out, void* stream);
 
+/* ---- FP32 roofline probe ----------------------------------------------------
+ * blocks x 256 threads, each running iters x 128 dependent-free FFMAs; the
+ * bench times it with CUDA events to measure the FP32 SIMT peak. */
+int fp_peak_ffma(int blocks, int iters, float* out, void* stream);
+
 /* ---- bookkeeping ---------------------------------------------------------- */
 /* Number of kernels this library has launched in the process (monotone). */
 uint64_t fp_launch_count(void);

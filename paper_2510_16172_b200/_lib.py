@@ -64,6 +64,7 @@ _SIGS = {
     "fp_objective_f64": [_P] * 5 + [_I64, _I] + [_P] * 4 + [_P],
     "fp_line_search_f64": [_P] * 7 + [_I64, _I, _I] + [_P] * 2 + [_P],
     "fp_init_params_f64": [_P] * 4 + [_I64, _I, _P, _P],
+    "fp_peak_ffma": [_I, _I, _P, _P],
     "fp_launch_count": [],
     "fp_last_cuda_error": [],
     "fp_error_string": [_I],

@@ -1,0 +1,39 @@
+// FP32 FFMA throughput microbenchmark: the measured SIMT roofline peak.
+//
+// MEASURED_PEAKS.json carries HBM and tensor-core peaks only; the Fermat
+// kernels are FP32-pipe bound, so bench.py measures this peak on the same
+// GPU in the same run. Every thread runs 16 independent FFMA chains (enough
+// ILP to cover the 4-cycle FMA latency at full occupancy).
+#include <cuda_runtime.h>
+
+#include "../../include/fermat_b200.h"
+#include "fp_dispatch.h"
+
+namespace fp {
+
+__global__ void __launch_bounds__(256) ffma_peak_kernel(int iters, float seed, float* out) {
+  float acc[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) acc[j] = seed + float(threadIdx.x + j);
+  const float x = 0.999999f + seed * 1e-9f, y = 1e-7f;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc[j] = fmaf(acc[j], x, y);
+    }
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) s += acc[j];
+  if (s == 1234.5f) out[0] = s;  // keep the chains alive
+}
+
+}  // namespace fp
+
+extern "C" int fp_peak_ffma(int blocks, int iters, float* out, void* stream) {
+  if (blocks < 1 || iters < 1) return FP_ERR_INVALID_ARGUMENT;
+  fp::ffma_peak_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(iters, 0.5f, out);
+  fp::count_launches(1);
+  return cudaGetLastError() == cudaSuccess ? FP_OK : FP_ERR_CUDA;
+}
