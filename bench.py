@@ -135,14 +135,16 @@ def _barrier(ws):
         dist.barrier()
 
 
-def _load_ncu_traffic(K: int):
+def _load_ncu_traffic(K: int, paths: int):
+    """DRAM bytes (read + write) per launch of the fused kernel, from the committed
+    `ncu --set full` capture (profiles/ncu_summary.json), scaled per path."""
     path = os.path.join(REPO, "profiles", "ncu_summary.json")
     try:
         with open(path) as fh:
             d = json.load(fh)
         ent = d.get(f"fused_k{K}")
-        return None if ent is None else ent.get("dram_bytes_per_launch")
-    except (OSError, ValueError):
+        return None if ent is None else float(ent["dram_bytes_per_path"]) * paths
+    except (OSError, ValueError, KeyError):
         return None
 
 
@@ -241,6 +243,7 @@ def run_ours(args):
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
     lib = _lib.load()
+    _lib.set_kernel_policy(args.policy)
     K, I, F = args.order, args.iterations, 1
     B = args.paths
     host = datagen.gen_batch(100 + K + 1000 * rank, datagen.all_orderings(K), B // 2 ** K)
@@ -324,7 +327,7 @@ def run_ours(args):
     except (OSError, ValueError):
         pass
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    traffic = _load_ncu_traffic(K)
+    traffic = _load_ncu_traffic(K, B)
 
     # ---- end to end through the host-buffer C-ABI entry ---------------------------------
     e2e = None
@@ -428,6 +431,8 @@ def main(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="tiny CPU samples (debugging)")
+    ap.add_argument("--policy", choices=("auto", "dense"), default="auto",
+                    help="kernel selection (fp_set_kernel_policy)")
     args = ap.parse_args(argv)
     if args.impl == "reference":
         return run_reference(args)

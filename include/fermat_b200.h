@@ -142,6 +142,14 @@ int fp_init_params_f64(const double* basis, const double* anchor, const double* 
 int fp_peak_ffma(int blocks, int iters, float* out, void* stream);
 
 /* ---- bookkeeping ---------------------------------------------------------- */
+/* Kernel selection: FP_POLICY_AUTO (default) buckets fp32 batches of order
+ * <= 5 by interaction-kind mask on the device and runs kernels that carry
+ * only the active unknowns; FP_POLICY_DENSE always runs the uniform 2K
+ * kernel (identical results, used by the tests to prove it). */
+#define FP_POLICY_AUTO 0
+#define FP_POLICY_DENSE 1
+int fp_set_kernel_policy(int policy);
+
 /* Number of kernels this library has launched in the process (monotone). */
 uint64_t fp_launch_count(void);
 /* Last CUDA error seen by the library (cudaError_t as int). */

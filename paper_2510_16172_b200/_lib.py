@@ -13,7 +13,8 @@ import re
 
 from .errors import FermatPathError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libfermat_b200.so")
+LIB_PATH = os.environ.get("FERMAT_B200_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "lib", "libfermat_b200.so")
 HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                       "include", "fermat_b200.h")
 
@@ -65,6 +66,7 @@ _SIGS = {
     "fp_line_search_f64": [_P] * 7 + [_I64, _I, _I] + [_P] * 2 + [_P],
     "fp_init_params_f64": [_P] * 4 + [_I64, _I, _P, _P],
     "fp_peak_ffma": [_I, _I, _P, _P],
+    "fp_set_kernel_policy": [_I],
     "fp_launch_count": [],
     "fp_last_cuda_error": [],
     "fp_error_string": [_I],
@@ -113,6 +115,16 @@ def check(rc: int, what: str) -> None:
     if rc == FP_ERR_INVALID_ARGUMENT:
         raise ValueError(f"{what}: {msg}")
     raise CudaCallError(f"{what}: {msg} (code {rc})")
+
+
+POLICY_AUTO = 0
+POLICY_DENSE = 1
+
+
+def set_kernel_policy(policy: str) -> None:
+    """'auto' (kind-mask specialised kernels, default) or 'dense' (uniform 2K kernel)."""
+    code = {"auto": POLICY_AUTO, "dense": POLICY_DENSE}[policy]
+    check(load().fp_set_kernel_policy(code), "fp_set_kernel_policy")
 
 
 def launch_count() -> int:

@@ -27,9 +27,10 @@ LIB = os.path.join(OUT_DIR, "libfermat_b200.so")
 OBJ_DIR = os.path.join(REPO, "build", "obj")
 
 ORDERS = range(1, 9)
+SPECIALISED_MAX_ORDER = 5  # fp_bucket.h kMaxSpecialisedOrder
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [
-    "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
+    "-O3", "-std=c++17", "-lineinfo", "-fmad=false", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
     "--expt-relaxed-constexpr", "-I", INCLUDE, "-I", CSRC,
 ]
 
@@ -53,21 +54,27 @@ def _sources_digest() -> str:
     return h.hexdigest()
 
 
-def _units():
-    units = [(os.path.join(CSRC, "fp_abi.cu"), os.path.join(OBJ_DIR, "fp_abi.o"), [])]
-    for k in ORDERS:
-        units.append((os.path.join(CSRC, "fp_inst.cu"), os.path.join(OBJ_DIR, f"fp_inst_k{k}.o"),
-                      [f"-DFP_INST_K={k}"]))
+def _units(orders=ORDERS, obj_dir=None):
+    obj_dir = obj_dir or OBJ_DIR
+    units = [(os.path.join(CSRC, "fp_abi.cu"), os.path.join(obj_dir, "fp_abi.o"), [])]
+    inst = os.path.join(CSRC, "fp_inst.cu")
+    for k in orders:
+        parts = (0, 1, 2) if k <= SPECIALISED_MAX_ORDER else (0,)
+        for part in parts:
+            units.append((inst, os.path.join(obj_dir, f"fp_inst_k{k}_p{part}.o"),
+                          [f"-DFP_INST_K={k}", f"-DFP_INST_PART={part}"]))
     for extra in ("fp_enum.cu", "fp_bucket.cu", "fp_peak.cu"):
         path = os.path.join(CSRC, extra)
         if os.path.exists(path):
-            units.append((path, os.path.join(OBJ_DIR, extra.replace(".cu", ".o")), []))
+            units.append((path, os.path.join(obj_dir, extra.replace(".cu", ".o")), []))
+    # longest units first so the parallel build finishes sooner
+    units.sort(key=lambda u: -sum(int(d.split("=")[1]) for d in u[2] if "FP_INST_K" in d))
     return units
 
 
-def _compile(unit):
+def _compile(unit, extra=()):
     src, obj, defs = unit
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *defs, "-c", src, "-o", obj]
+    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *extra, *defs, "-c", src, "-o", obj]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed for {os.path.basename(obj)}:\n{res.stderr}")
@@ -101,11 +108,56 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -
     return LIB
 
 
+def build_variant(out: str, orders, defines=(), jobs=None) -> str:
+    """Experimental library (subset of orders, extra -D flags) for A/B timing.
+
+    Loaded instead of the default one with FERMAT_B200_LIB=<out>.
+    """
+    tag = os.path.splitext(os.path.basename(out))[0]
+    obj_dir = os.path.join(REPO, "build", "variants", tag)
+    os.makedirs(obj_dir, exist_ok=True)
+    os.makedirs(os.path.dirname(os.path.abspath(out)), exist_ok=True)
+    extra = [f"-D{d}" for d in defines]
+    orders = list(orders)
+    units = _units(orders, obj_dir)
+    # orders missing from the variant still need their dispatch symbols: stub them
+    stub = os.path.join(obj_dir, "stub.cu")
+    with open(stub, "w") as fh:
+        fh.write('#include "fp_kernels.cuh"\n#include "fp_dispatch.h"\nnamespace fp {\n')
+        for k in ORDERS:
+            if k in orders:
+                continue
+            for R in ("float", "double"):
+                fh.write(f"template <> cudaError_t dispatch_dense<{R}, {k}>(const PathArgs<{R}>&, int, "
+                         "cudaStream_t) { return cudaErrorNotSupported; }\n")
+            if k <= SPECIALISED_MAX_ORDER:
+                for fn in ("dispatch_masked_solve", "dispatch_masked_solve_vjp"):
+                    fh.write(f"template <> cudaError_t {fn}<{k}>(const PathArgs<float>&, unsigned, "
+                             "cudaStream_t) { return cudaErrorNotSupported; }\n")
+        fh.write("}\n")
+    units.append((stub, os.path.join(obj_dir, "stub.o"), []))
+    jobs = jobs or min(len(units), os.cpu_count() or 4)
+    with cf.ThreadPoolExecutor(max_workers=jobs) as ex:
+        objs = list(ex.map(lambda u: _compile(u, extra), units))
+    cmd = [nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", out, *objs, "-lcudart_static"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"link failed:\n{res.stderr}")
+    return out
+
+
 def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("-j", type=int, default=None)
+    ap.add_argument("--variant", help="output path of an experimental library")
+    ap.add_argument("--orders", default="3", help="comma list of orders for --variant")
+    ap.add_argument("-D", dest="defines", action="append", default=[])
     args = ap.parse_args(argv)
+    if args.variant:
+        print(build_variant(args.variant, [int(k) for k in args.orders.split(",")], args.defines,
+                            args.j))
+        return
     build(force=args.force, jobs=args.j, verbose=True)
 
 

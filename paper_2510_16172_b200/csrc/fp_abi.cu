@@ -10,6 +10,7 @@
 #include <mutex>
 #include <vector>
 
+#include "fp_bucket.h"
 #include "fp_dispatch.h"
 #include "fp_kernels.cuh"
 
@@ -60,22 +61,65 @@ static int run_order0(const R* start, const R* end, int64_t B, R* length_out, co
   return cuda_status(cudaGetLastError());
 }
 
+static std::atomic<int> g_policy{FP_POLICY_AUTO};
+
 template <typename R>
-static int dispatch(int K, const PathArgs<R>& a, int op, cudaStream_t s) {
+static int dispatch_dense_k(int K, const PathArgs<R>& a, int op, cudaStream_t s) {
   cudaError_t e;
   switch (K) {
-    case 1: e = dispatch_k<R, 1>(a, op, 0u, s); break;
-    case 2: e = dispatch_k<R, 2>(a, op, 0u, s); break;
-    case 3: e = dispatch_k<R, 3>(a, op, 0u, s); break;
-    case 4: e = dispatch_k<R, 4>(a, op, 0u, s); break;
-    case 5: e = dispatch_k<R, 5>(a, op, 0u, s); break;
-    case 6: e = dispatch_k<R, 6>(a, op, 0u, s); break;
-    case 7: e = dispatch_k<R, 7>(a, op, 0u, s); break;
-    case 8: e = dispatch_k<R, 8>(a, op, 0u, s); break;
+    case 1: e = dispatch_dense<R, 1>(a, op, s); break;
+    case 2: e = dispatch_dense<R, 2>(a, op, s); break;
+    case 3: e = dispatch_dense<R, 3>(a, op, s); break;
+    case 4: e = dispatch_dense<R, 4>(a, op, s); break;
+    case 5: e = dispatch_dense<R, 5>(a, op, s); break;
+    case 6: e = dispatch_dense<R, 6>(a, op, s); break;
+    case 7: e = dispatch_dense<R, 7>(a, op, s); break;
+    case 8: e = dispatch_dense<R, 8>(a, op, s); break;
     default: return FP_ERR_UNSUPPORTED_ORDER;
   }
-  if ((a.rows ? a.n_rows : a.B) > 0) count_launches(1);
+  if (a.B > 0) count_launches(1);
   return cuda_status(e);
+}
+
+static cudaError_t masked_k(int K, const PathArgs<float>& a, int op, unsigned m, cudaStream_t s) {
+  const bool v = op == OP_SOLVE_VJP;
+  switch (K) {
+    case 1: return v ? dispatch_masked_solve_vjp<1>(a, m, s) : dispatch_masked_solve<1>(a, m, s);
+    case 2: return v ? dispatch_masked_solve_vjp<2>(a, m, s) : dispatch_masked_solve<2>(a, m, s);
+    case 3: return v ? dispatch_masked_solve_vjp<3>(a, m, s) : dispatch_masked_solve<3>(a, m, s);
+    case 4: return v ? dispatch_masked_solve_vjp<4>(a, m, s) : dispatch_masked_solve<4>(a, m, s);
+    case 5: return v ? dispatch_masked_solve_vjp<5>(a, m, s) : dispatch_masked_solve<5>(a, m, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// fp32 solve / fused step for K <= 5: bucket paths by kind mask on the
+// device, then one specialised kernel per mask (empty buckets exit at once).
+template <typename R>
+static int dispatch(int K, const PathArgs<R>& a, int op, cudaStream_t s) {
+  constexpr bool is_f32 = sizeof(R) == sizeof(float);
+  const bool bucketed = is_f32 && g_policy.load() == FP_POLICY_AUTO && K >= 1 &&
+                        K <= kMaxSpecialisedOrder && (op == OP_SOLVE || op == OP_SOLVE_VJP) &&
+                        a.B > 0 && a.B < (int64_t(1) << 31);
+  if (!bucketed) return dispatch_dense_k<R>(K, a, op, s);
+  if constexpr (is_f32) {
+    BucketScratch sc;
+    cudaError_t e = bucket_rows<float>(a.basis, a.B, K, sc, s);
+    if (e != cudaSuccess) {
+      bucket_free(sc, s);
+      return cuda_status(e);
+    }
+    PathArgs<float> b = a;
+    b.rows = sc.rows;
+    for (unsigned m = 0; m < (1u << K) && e == cudaSuccess; ++m) {
+      b.bucket = sc.buckets + 2 * m;
+      e = masked_k(K, b, op, m, s);
+      count_launches(1);
+    }
+    bucket_free(sc, s);
+    return cuda_status(e);
+  }
+  return FP_ERR_INVALID_ARGUMENT;
 }
 
 template <typename R>
@@ -515,6 +559,12 @@ int fp_init_params_f64(const double* basis, const double* anchor, const double* 
 }
 
 uint64_t fp_launch_count(void) { return g_launches.load(); }
+
+int fp_set_kernel_policy(int policy) {
+  if (policy != FP_POLICY_AUTO && policy != FP_POLICY_DENSE) return FP_ERR_INVALID_ARGUMENT;
+  g_policy.store(policy);
+  return FP_OK;
+}
 int fp_last_cuda_error(void) { return g_last_cuda.load(); }
 
 const char* fp_error_string(int code) {

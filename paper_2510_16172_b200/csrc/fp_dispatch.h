@@ -9,9 +9,16 @@ namespace fp {
 template <typename R>
 struct PathArgs;
 
-// Defined in fp_inst.cu, one explicit specialisation per (R, K).
+// Dense (uniform 2K) kernels, every op; defined in fp_inst.cu (part 0).
 template <typename R, int K>
-cudaError_t dispatch_k(const PathArgs<R>& a, int op, unsigned mask, cudaStream_t s);
+cudaError_t dispatch_dense(const PathArgs<R>& a, int op, cudaStream_t s);
+
+// Kind-mask specialised fp32 kernels for K <= 5; fp_inst.cu parts 1 (solve)
+// and 2 (fused solve + VJP).
+template <int K>
+cudaError_t dispatch_masked_solve(const PathArgs<float>& a, unsigned mask, cudaStream_t s);
+template <int K>
+cudaError_t dispatch_masked_solve_vjp(const PathArgs<float>& a, unsigned mask, cudaStream_t s);
 
 void count_launches(uint64_t n);
 

@@ -1,10 +1,16 @@
-// Per-order instantiation unit: compiled once per K (-DFP_INST_K=K) so the
-// heavy unrolled kernels of different orders build in parallel.
+// Per-order instantiation unit, compiled once per (K, part) so the heavy
+// unrolled kernels build in parallel:
+//   -DFP_INST_K=K -DFP_INST_PART=0   dense kernels (fp32 + fp64, every op)
+//   -DFP_INST_PART=1 / 2             kind-mask specialised fp32 solve /
+//                                    fused solve + VJP, one kernel per mask
 #include "fp_dispatch.h"
 #include "fp_kernels.cuh"
 
 #ifndef FP_INST_K
 #error "compile with -DFP_INST_K=<order>"
+#endif
+#ifndef FP_INST_PART
+#define FP_INST_PART 0
 #endif
 
 namespace fp {
@@ -13,28 +19,47 @@ namespace {
 constexpr int kK = FP_INST_K;
 constexpr unsigned kDense = (1u << kK) - 1u;
 
-template <typename R, unsigned MASK>
-cudaError_t by_op(const PathArgs<R>& a, int op, cudaStream_t s) {
+template <typename R>
+cudaError_t dense_by_op(const PathArgs<R>& a, int op, cudaStream_t s) {
   switch (op) {
-    case OP_SOLVE: return launch_path_impl<R, kK, MASK, OP_SOLVE>(a, s);
-    case OP_SOLVE_VJP: return launch_path_impl<R, kK, MASK, OP_SOLVE_VJP>(a, s);
-    case OP_VJP: return launch_path_impl<R, kK, MASK, OP_VJP>(a, s);
+    case OP_SOLVE: return launch_path_impl<R, kK, kDense, OP_SOLVE>(a, s);
+    case OP_SOLVE_VJP: return launch_path_impl<R, kK, kDense, OP_SOLVE_VJP>(a, s);
+    case OP_VJP: return launch_path_impl<R, kK, kDense, OP_VJP>(a, s);
     default: return cudaErrorInvalidValue;
+  }
+}
+
+// Compile-time chain over every mask 0 .. 2^K - 1.
+template <int OP, unsigned M>
+cudaError_t by_mask(unsigned mask, const PathArgs<float>& a, cudaStream_t s) {
+  if (mask == M) return launch_path_impl<float, kK, M, OP>(a, s);
+  if constexpr (M + 1 < (1u << kK)) {
+    return by_mask<OP, M + 1>(mask, a, s);
+  } else {
+    return cudaErrorInvalidValue;
   }
 }
 }  // namespace
 
-
+#if FP_INST_PART == 0
 template <>
-cudaError_t dispatch_k<float, kK>(const PathArgs<float>& a, int op, unsigned mask, cudaStream_t s) {
-  (void)mask;
-  return by_op<float, kDense>(a, op, s);
+cudaError_t dispatch_dense<float, kK>(const PathArgs<float>& a, int op, cudaStream_t s) {
+  return dense_by_op<float>(a, op, s);
 }
-
 template <>
-cudaError_t dispatch_k<double, kK>(const PathArgs<double>& a, int op, unsigned mask, cudaStream_t s) {
-  (void)mask;
-  return by_op<double, kDense>(a, op, s);
+cudaError_t dispatch_dense<double, kK>(const PathArgs<double>& a, int op, cudaStream_t s) {
+  return dense_by_op<double>(a, op, s);
 }
+#elif FP_INST_PART == 1
+template <>
+cudaError_t dispatch_masked_solve<kK>(const PathArgs<float>& a, unsigned mask, cudaStream_t s) {
+  return by_mask<OP_SOLVE, 0u>(mask, a, s);
+}
+#elif FP_INST_PART == 2
+template <>
+cudaError_t dispatch_masked_solve_vjp<kK>(const PathArgs<float>& a, unsigned mask, cudaStream_t s) {
+  return by_mask<OP_SOLVE_VJP, 0u>(mask, a, s);
+}
+#endif
 
 }  // namespace fp

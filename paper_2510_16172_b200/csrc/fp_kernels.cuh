@@ -30,8 +30,10 @@ struct PathArgs {
   uint8_t* status_out;
   R *trace_len, *trace_gnorm, *H_out;
   R *d_basis, *d_anchor, *d_start, *d_end, *u_out;
-  const int32_t* rows;  // optional row indirection (length n_rows)
-  int64_t n_rows;
+  // Bucketed dispatch (fp_bucket.cu): rows[bucket[0] + i], i < bucket[1],
+  // are this launch's paths; both live in device memory.
+  const int32_t* rows;
+  const int64_t* bucket;
 };
 
 // Per-path output destinations (shared-memory slab slots or global records).
@@ -40,6 +42,63 @@ struct Outs {
   R *T, *g, *pts, *len, *db, *da, *d0, *d1, *u;
   uint8_t* st;
 };
+
+// Widths (elements per path) of the staged slabs.
+template <int K>
+struct W {
+  static constexpr int basis = 6 * K, anchor = 3 * K, vec = 3, T = 2 * K, pts = 3 * K;
+  static constexpr int in_elems = basis + anchor + 2 * vec + 2 * T;                   // + vT
+  static constexpr int out_elems = 2 * T + pts + 1 + basis + anchor + 2 * vec + T;  // T g pts len db da d0 d1 u
+  static constexpr int slab_elems = in_elems > out_elems ? in_elems : out_elems;
+};
+
+template <typename R, int K>
+constexpr size_t smem_bytes() {
+  return size_t(W<K>::slab_elems) * kThreads * sizeof(R) + kThreads + 16;
+}
+
+extern __shared__ __align__(16) unsigned char fp_smem[];
+
+// Output destinations of one path, computed only when results are written
+// (keeps ten 64-bit pointers out of the registers live across the solve).
+template <typename R, int K>
+__device__ __forceinline__ Outs<R> make_outs(const PathArgs<R>& a, int64_t row, int tid, bool staged) {
+  using Wk = W<K>;
+  Outs<R> o;
+  if (!staged) {
+    o.T = a.T_out ? a.T_out + row * Wk::T : nullptr;
+    o.g = a.g_out ? a.g_out + row * Wk::T : nullptr;
+    o.pts = a.points_out ? a.points_out + row * Wk::pts : nullptr;
+    o.len = a.length_out ? a.length_out + row : nullptr;
+    o.db = a.d_basis ? a.d_basis + row * Wk::basis : nullptr;
+    o.da = a.d_anchor ? a.d_anchor + row * Wk::anchor : nullptr;
+    o.d0 = a.d_start ? a.d_start + row * 3 : nullptr;
+    o.d1 = a.d_end ? a.d_end + row * 3 : nullptr;
+    o.u = a.u_out ? a.u_out + row * Wk::T : nullptr;
+    o.st = a.status_out ? a.status_out + row : nullptr;
+    return o;
+  }
+  R* oT = reinterpret_cast<R*>(fp_smem);
+  R* og = oT + kThreads * Wk::T;
+  R* op = og + kThreads * Wk::T;
+  R* ol = op + kThreads * Wk::pts;
+  R* odb = ol + kThreads;
+  R* oda = odb + kThreads * Wk::basis;
+  R* od0 = oda + kThreads * Wk::anchor;
+  R* od1 = od0 + kThreads * 3;
+  R* ou = od1 + kThreads * 3;
+  o.T = a.T_out ? oT + tid * Wk::T : nullptr;
+  o.g = a.g_out ? og + tid * Wk::T : nullptr;
+  o.pts = a.points_out ? op + tid * Wk::pts : nullptr;
+  o.len = a.length_out ? ol + tid : nullptr;
+  o.db = a.d_basis ? odb + tid * Wk::basis : nullptr;
+  o.da = a.d_anchor ? oda + tid * Wk::anchor : nullptr;
+  o.d0 = a.d_start ? od0 + tid * 3 : nullptr;
+  o.d1 = a.d_end ? od1 + tid * 3 : nullptr;
+  o.u = a.u_out ? ou + tid * Wk::T : nullptr;
+  o.st = reinterpret_cast<uint8_t*>(fp_smem + size_t(Wk::slab_elems) * kThreads * sizeof(R)) + tid;
+  return o;
+}
 
 // ---- TMA bulk copy helpers -------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -109,7 +168,7 @@ __device__ __forceinline__ void load_rec(Rec<R, K>& r, const R* b, const R* a, c
 // ---- the per-path body -------------------------------------------------------
 template <typename R, int K, unsigned MASK, int OP>
 __device__ __forceinline__ void run_path(const PathArgs<R>& a, int64_t row, const Rec<R, K>& in,
-                                         bool has_v, const Outs<R>& o) {
+                                         bool has_v, int tid, bool staged) {
   using L = Lay<K, MASK>;
   constexpr int NA = L::NA;
   Geo<R, K> G;
@@ -153,7 +212,7 @@ __device__ __forceinline__ void run_path(const PathArgs<R>& a, int64_t row, cons
         ss = fma(sg[j], sg[j], ss);
         yy = fma(y[j], y[j], yy);
       }
-      const bool ok = sy > (R(1e-12) * Num<R>::sqrt_(ss)) * Num<R>::sqrt_(yy);
+      const bool ok = sy > (R(1e-12) * sqrt_test(ss)) * sqrt_test(yy);
       if (ok) H.update(sg, y, Num<R>::rcp(sy));
 #pragma unroll
       for (int j = 0; j < NA; ++j) P.g[j] = gn[j];
@@ -193,6 +252,7 @@ __device__ __forceinline__ void run_path(const PathArgs<R>& a, int64_t row, cons
     tf[i][0] = P.t[L::idx(i, 0)];
     tf[i][1] = L::plane(i) ? P.t[L::idx(i, 1)] : tin[i];
   }
+  const Outs<R> o = make_outs<R, K>(a, row, tid, staged);
   if (OP != OP_VJP) {
     if (o.T)
 #pragma unroll
@@ -256,52 +316,34 @@ __device__ __forceinline__ void run_path(const PathArgs<R>& a, int64_t row, cons
   if (o.st) o.st[0] = st;
 }
 
-// Widths (elements per path) of the staged slabs.
-template <int K>
-struct W {
-  static constexpr int basis = 6 * K, anchor = 3 * K, vec = 3, T = 2 * K, pts = 3 * K;
-  static constexpr int in_elems = basis + anchor + 2 * vec + 2 * T;                   // + vT
-  static constexpr int out_elems = 2 * T + pts + 1 + basis + anchor + 2 * vec + T;  // T g pts len db da d0 d1 u
-  static constexpr int slab_elems = in_elems > out_elems ? in_elems : out_elems;
-};
-
-template <typename R, int K>
-constexpr size_t smem_bytes() {
-  return size_t(W<K>::slab_elems) * kThreads * sizeof(R) + kThreads + 16;
-}
-
 template <typename R, int K, unsigned MASK, int OP>
-__global__ void __launch_bounds__(kThreads) path_kernel(const PathArgs<R> a) {
-  extern __shared__ __align__(16) unsigned char smem[];
+#ifndef FP_MIN_BLOCKS
+#define FP_MIN_BLOCKS 1
+#endif
+__global__ void __launch_bounds__(kThreads, FP_MIN_BLOCKS) path_kernel(const PathArgs<R> a) {
+  unsigned char* smem = fp_smem;
   __shared__ __align__(8) uint64_t bar;
   using Wk = W<K>;
   const int tid = threadIdx.x;
-  const int64_t base = int64_t(blockIdx.x) * kThreads;
-  const int64_t total = a.rows ? a.n_rows : a.B;
-  if (base >= total) return;
-  const int n = int(total - base < kThreads ? total - base : int64_t(kThreads));
-
   if (a.rows != nullptr) {
-    // Bucketed dispatch: direct per-thread records.
-    if (tid >= n) return;
-    const int64_t row = a.rows[base + tid];
-    Outs<R> o;
-    o.T = a.T_out ? a.T_out + row * Wk::T : nullptr;
-    o.g = a.g_out ? a.g_out + row * Wk::T : nullptr;
-    o.pts = a.points_out ? a.points_out + row * Wk::pts : nullptr;
-    o.len = a.length_out ? a.length_out + row : nullptr;
-    o.db = a.d_basis ? a.d_basis + row * Wk::basis : nullptr;
-    o.da = a.d_anchor ? a.d_anchor + row * Wk::anchor : nullptr;
-    o.d0 = a.d_start ? a.d_start + row * 3 : nullptr;
-    o.d1 = a.d_end ? a.d_end + row * 3 : nullptr;
-    o.u = a.u_out ? a.u_out + row * Wk::T : nullptr;
-    o.st = a.status_out ? a.status_out + row : nullptr;
-    Rec<R, K> in;
-    load_rec(in, a.basis + row * Wk::basis, a.anchor + row * Wk::anchor, a.start + row * 3,
-             a.end + row * 3, a.T + row * Wk::T, a.vT ? a.vT + row * Wk::T : nullptr);
-    run_path<R, K, MASK, OP>(a, row, in, a.vT != nullptr, o);
+    // Bucketed dispatch: persistent grid-stride over this bucket's rows,
+    // direct per-thread records (each record is one contiguous run).
+    const int64_t off = a.bucket[0], cnt = a.bucket[1];
+    for (int64_t i = int64_t(blockIdx.x) * kThreads + tid; i - tid < cnt;
+         i += int64_t(gridDim.x) * kThreads) {
+      if (i >= cnt) continue;
+      const int64_t row = a.rows[off + i];
+      Rec<R, K> in;
+      load_rec(in, a.basis + row * Wk::basis, a.anchor + row * Wk::anchor, a.start + row * 3,
+               a.end + row * 3, a.T + row * Wk::T, a.vT ? a.vT + row * Wk::T : nullptr);
+      run_path<R, K, MASK, OP>(a, row, in, a.vT != nullptr, tid, false);
+    }
     return;
   }
+  const int64_t base = int64_t(blockIdx.x) * kThreads;
+  const int64_t total = a.B;
+  if (base >= total) return;
+  const int n = int(total - base < kThreads ? total - base : int64_t(kThreads));
 
   // ---- stage the CTA's input slabs -----------------------------------------
   R* sb = reinterpret_cast<R*>(smem);
@@ -364,18 +406,7 @@ __global__ void __launch_bounds__(kThreads) path_kernel(const PathArgs<R> a) {
              sT + tid * Wk::T, gv ? sv + tid * Wk::T : nullptr);
   __syncthreads();
   if (tid < n) {
-    Outs<R> o;
-    o.T = a.T_out ? oT + tid * Wk::T : nullptr;
-    o.g = a.g_out ? og + tid * Wk::T : nullptr;
-    o.pts = a.points_out ? op + tid * Wk::pts : nullptr;
-    o.len = a.length_out ? ol + tid : nullptr;
-    o.db = a.d_basis ? odb + tid * Wk::basis : nullptr;
-    o.da = a.d_anchor ? oda + tid * Wk::anchor : nullptr;
-    o.d0 = a.d_start ? od0 + tid * 3 : nullptr;
-    o.d1 = a.d_end ? od1 + tid * 3 : nullptr;
-    o.u = a.u_out ? ou + tid * Wk::T : nullptr;
-    o.st = ost + tid;
-    run_path<R, K, MASK, OP>(a, base + tid, in, gv != nullptr, o);
+    run_path<R, K, MASK, OP>(a, base + tid, in, gv != nullptr, tid, true);
   }
   __syncthreads();
 
@@ -398,17 +429,22 @@ cudaError_t launch_path(const PathArgs<R>& a, cudaStream_t stream);
 
 template <typename R, int K, unsigned MASK, int OP>
 cudaError_t launch_path_impl(const PathArgs<R>& a, cudaStream_t stream) {
-  const int64_t total = a.rows ? a.n_rows : a.B;
-  if (total <= 0) return cudaSuccess;
-  const size_t smem = smem_bytes<R, K>();
-  static bool configured = false;
-  if (!configured) {
+  if (a.B <= 0) return cudaSuccess;
+  const size_t smem = a.rows ? 0 : smem_bytes<R, K>();
+  static int resident = 0;  // co-resident CTAs on the whole GPU (bucketed launches)
+  if (resident == 0) {
     cudaError_t e = cudaFuncSetAttribute(path_kernel<R, K, MASK, OP>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(smem_bytes<R, K>()));
     if (e != cudaSuccess) return e;
-    configured = true;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, path_kernel<R, K, MASK, OP>, kThreads, 0);
+    resident = (sms > 0 ? sms : 148) * (per_sm > 0 ? per_sm : 1);
   }
-  const int64_t blocks = (total + kThreads - 1) / kThreads;
+  int64_t blocks = (a.B + kThreads - 1) / kThreads;
+  if (a.rows != nullptr && blocks > resident) blocks = resident;
   path_kernel<R, K, MASK, OP><<<dim3(unsigned(blocks)), dim3(kThreads), smem, stream>>>(a);
   return cudaGetLastError();
 }

@@ -27,6 +27,7 @@ struct Geo {
   R b[K][3];     // anchor
   R x0[3], xe[3];
   R eps;         // 1e-12 (1 + |end - start|), fp64 then cast (batching.py:67-72)
+  R reps;        // 1 / eps
 };
 
 // Load one path's geometry from a record in the reference layout.
@@ -53,6 +54,7 @@ __device__ __forceinline__ void load_geo(Geo<R, K>& G, const R* basis, const R* 
   const double dz = double(G.xe[2]) - double(G.x0[2]);
   const double nrm = __dsqrt_rn(__fma_rn(dz, dz, __fma_rn(dy, dy, dx * dx)));
   G.eps = R(1e-12 * (1.0 + nrm));
+  G.reps = Num<R>::rcp(G.eps);
 }
 
 template <typename R, int K, unsigned MASK>
@@ -101,11 +103,10 @@ struct PathState {
       R q = s[k][0] * s[k][0];
       q = fma(s[k][1], s[k][1], q);
       q = fma(s[k][2], s[k][2], q);
-      const R n = Num<R>::sqrt_(q);
+      R n;
+      norm_rcp(q, G.eps, G.reps, n, nc[k], rn[k]);
       len += n;
       nmin = n < nmin ? n : nmin;
-      nc[k] = clamp_floor(n, G.eps);
-      rn[k] = Num<R>::rcp(nc[k]);
 #pragma unroll
       for (int r = 0; r < 3; ++r) u[k][r] = s[k][r] * rn[k];
     }
@@ -174,8 +175,8 @@ struct PathState {
         const R e0 = fma(alpha, d[k][0], s[k][0]);
         const R e1 = fma(alpha, d[k][1], s[k][1]);
         const R e2 = fma(alpha, d[k][2], s[k][2]);
-        const R n = clamp_floor(Num<R>::sqrt_(fma(e2, e2, fma(e1, e1, e0 * e0))), G.eps);
-        const R ri = Num<R>::rcp(n);
+        R n0, n, ri;
+        norm_rcp(fma(e2, e2, fma(e1, e1, e0 * e0)), G.eps, G.reps, n0, n, ri);
         num = fma(c[k], ri, num);
         den = fma(a2[k], ri, den);
       }

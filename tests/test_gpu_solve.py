@@ -210,3 +210,28 @@ def test_launch_counter_advances():
           SolveOptions(iterations=10, precision=Precision.SINGLE))
     torch.cuda.synchronize()
     assert _lib.launch_count() == before + 1
+
+
+@pytest.mark.parametrize("K", [2, 3, 5])
+def test_specialised_kernels_match_dense_bitwise(K):
+    """Kind-mask specialised kernels (bucketed dispatch) == the uniform 2K kernel, bit for bit."""
+    from paper_2510_16172_b200.solver import solve_with_gradients
+
+    b = datagen.interleave(datagen.gen_batch(21, datagen.all_orderings(K), 97), seed=K)
+    sc = BatchScene(b.basis, b.anchor, b.start, b.end)
+    opts = SolveOptions(iterations=20, precision=Precision.SINGLE, record_trace=True)
+    try:
+        _lib.set_kernel_policy("dense")
+        dense = solve(sc, b.T0, opts)
+        dres, dgrad = solve_with_gradients(sc, b.T0, SolveOptions(iterations=20, precision=Precision.SINGLE))
+        _lib.set_kernel_policy("auto")
+        spec = solve(sc, b.T0, opts)
+        sres, sgrad = solve_with_gradients(sc, b.T0, SolveOptions(iterations=20, precision=Precision.SINGLE))
+    finally:
+        _lib.set_kernel_policy("auto")
+    for x, y in ((dense.T, spec.T), (dense.g, spec.g), (dense.points, spec.points),
+                 (dense.length, spec.length), (dense.status, spec.status),
+                 (dense.trace_len, spec.trace_len), (dense.trace_gnorm, spec.trace_gnorm),
+                 (dres.T, sres.T), (dgrad.basis, sgrad.basis), (dgrad.anchor, sgrad.anchor),
+                 (dgrad.start, sgrad.start), (dgrad.end, sgrad.end), (dres.status, sres.status)):
+        assert torch.equal(x, y)
