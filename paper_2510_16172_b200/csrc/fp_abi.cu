@@ -93,29 +93,44 @@ static cudaError_t masked_k(int K, const PathArgs<float>& a, int op, unsigned m,
   }
 }
 
-// fp32 solve / fused step for K <= 5: bucket paths by kind mask on the
-// device, then one specialised kernel per mask (empty buckets exit at once).
+// fp32 solve / fused step for K <= 5: classify paths by kind mask on the
+// device, then one specialised kernel per non-empty mask — the staged TMA
+// kernel on the mask's row range when it is contiguous, the gathering kernel
+// over a row permutation otherwise — on side streams so tails overlap.
 template <typename R>
 static int dispatch(int K, const PathArgs<R>& a, int op, cudaStream_t s) {
   constexpr bool is_f32 = sizeof(R) == sizeof(float);
+  const int64_t B = a.B;
   const bool bucketed = is_f32 && g_policy.load() == FP_POLICY_AUTO && K >= 1 &&
                         K <= kMaxSpecialisedOrder && (op == OP_SOLVE || op == OP_SOLVE_VJP) &&
-                        a.B > 0 && a.B < (int64_t(1) << 31);
+                        B > 0 && B < (int64_t(1) << 31) && a.rows == nullptr;
   if (!bucketed) return dispatch_dense_k<R>(K, a, op, s);
   if constexpr (is_f32) {
     BucketScratch sc;
-    cudaError_t e = bucket_rows<float>(a.basis, a.B, K, sc, s);
-    if (e != cudaSuccess) {
-      bucket_free(sc, s);
-      return cuda_status(e);
-    }
-    PathArgs<float> b = a;
-    b.rows = sc.rows;
-    for (unsigned m = 0; m < (1u << K) && e == cudaSuccess; ++m) {
-      b.bucket = sc.buckets + 2 * m;
-      e = masked_k(K, b, op, m, s);
+    BucketPlan plan;
+    cudaError_t e = bucket_plan<float>(a.basis, B, K, sc, plan, s);
+    if (e == cudaSuccess && !plan.all_contiguous) e = bucket_scatter(B, plan, sc, s);
+    int live = 0;
+    for (int m = 0; m < plan.nb; ++m) live += plan.count[m] > 0;
+    SideStreams& ss = side_streams();
+    const bool fan = live > 1;
+    if (e == cudaSuccess && fan) e = ss.fork(s, live);
+    int k = 0;
+    for (unsigned m = 0; m < unsigned(plan.nb) && e == cudaSuccess; ++m) {
+      if (plan.count[m] == 0) continue;
+      PathArgs<float> b = a;
+      if (plan.contiguous[m]) {
+        b.row_begin = plan.lo[m];
+        b.B = plan.hi[m] + 1;
+      } else {
+        b.rows = sc.rows + plan.offset[m];
+        b.n_rows = plan.count[m];
+      }
+      cudaStream_t st = fan ? ss.st[k++ % SideStreams::kSide] : s;
+      e = masked_k(K, b, op, m, st);
       count_launches(1);
     }
+    if (e == cudaSuccess && fan) e = ss.join(s);
     bucket_free(sc, s);
     return cuda_status(e);
   }
@@ -127,6 +142,12 @@ static PathArgs<R> blank_args() {
   PathArgs<R> a;
   std::memset(&a, 0, sizeof(a));
   return a;
+}
+
+template <typename R>
+static void finish_args(PathArgs<R>& a) {
+  a.row_begin = 0;
+  a.ld = a.B;
 }
 
 template <typename R>
@@ -148,6 +169,7 @@ static int solve_impl(const R* basis, const R* anchor, const R* start, const R* 
   a.B = B; a.iterations = iterations; a.fp_iters = fp_iters;
   a.T_out = T_out; a.g_out = g_out; a.points_out = points_out; a.length_out = length_out;
   a.status_out = status_out; a.trace_len = trace_len; a.trace_gnorm = trace_gnorm; a.H_out = H_out;
+  finish_args(a);
   return dispatch<R>(K, a, OP_SOLVE, s);
 }
 
@@ -168,6 +190,7 @@ static int vjp_impl(const R* basis, const R* anchor, const R* start, const R* en
   a.wL = w_L; a.wL_scale = w_L_scale; a.mode = mode; a.B = B; a.iterations = 1; a.fp_iters = 1;
   a.d_basis = d_basis; a.d_anchor = d_anchor; a.d_start = d_start; a.d_end = d_end;
   a.u_out = u_out; a.status_out = status_out;
+  finish_args(a);
   return dispatch<R>(K, a, OP_VJP, s);
 }
 
@@ -189,6 +212,7 @@ static int solve_vjp_impl(const R* basis, const R* anchor, const R* start, const
   a.T_out = T_out; a.points_out = points_out; a.length_out = length_out;
   a.d_basis = d_basis; a.d_anchor = d_anchor; a.d_start = d_start; a.d_end = d_end;
   a.status_out = status_out;
+  finish_args(a);
   return dispatch<R>(K, a, OP_SOLVE_VJP, s);
 }
 

@@ -2,10 +2,15 @@
 //
 // Each path's kind mask (bit i set when interaction i has a nonzero second
 // basis column, i.e. is a plane; geometry.py:74-77) selects a kernel
-// instantiation that carries only the active unknowns. One pass classifies
-// and histograms, a 32-thread pass turns counts into bucket ranges, and a
-// scatter pass writes the row permutation with warp-aggregated atomics (one
-// atomic per warp and mask). Everything stays on the device: no host sync.
+// instantiation that carries only the active unknowns.
+//
+//   1. classify: one pass writes each path's mask and, per mask, the count and
+//      the first/last row (warp-aggregated atomics); 2^K * 3 numbers come back
+//      to the host (one small copy + stream sync).
+//   2. masks whose rows form one contiguous range (config 2's ordering-major
+//      layout, uniform batches) run the staged TMA kernel on that sub-range;
+//   3. only if some mask is scattered, offsets + scatter build a row
+//      permutation and those masks run the gathering kernel.
 #include <cuda_runtime.h>
 
 #include "fp_bucket.h"
@@ -15,10 +20,16 @@ namespace fp {
 
 template <typename R>
 __global__ void classify_kernel(const R* __restrict__ basis, int64_t B, int K,
-                                uint8_t* __restrict__ codes, unsigned long long* __restrict__ counts) {
+                                uint8_t* __restrict__ codes, unsigned long long* __restrict__ stats) {
+  // stats: [0, nb) counts, [nb, 2nb) min row, [2nb, 3nb) max row
   __shared__ unsigned int hist[kMaxBuckets];
+  __shared__ unsigned long long lo[kMaxBuckets], hi[kMaxBuckets];
   const int nb = 1 << K;
-  for (int i = threadIdx.x; i < nb; i += blockDim.x) hist[i] = 0;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+    hist[i] = 0;
+    lo[i] = ~0ull;
+    hi[i] = 0;
+  }
   __syncthreads();
   for (int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; b - threadIdx.x < B;
        b += int64_t(gridDim.x) * blockDim.x) {
@@ -35,25 +46,34 @@ __global__ void classify_kernel(const R* __restrict__ basis, int64_t B, int K,
     const unsigned live_mask = __ballot_sync(0xffffffffu, live);
     if (live) {
       const unsigned same = __match_any_sync(live_mask, code);
+      const int lane = threadIdx.x & 31;
       const int leader = __ffs(same) - 1;
-      if ((threadIdx.x & 31) == leader) atomicAdd(&hist[code], unsigned(__popc(same)));
+      const int last = 31 - __clz(same);
+      // lanes are consecutive rows: the group's first/last rows are its end lanes
+      const unsigned long long first = __shfl_sync(same, (unsigned long long)b, leader);
+      const unsigned long long lastrow = __shfl_sync(same, (unsigned long long)b, last);
+      if (lane == leader) {
+        atomicAdd(&hist[code], unsigned(__popc(same)));
+        atomicMin(&lo[code], first);
+        atomicMax(&hi[code], lastrow);
+      }
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < nb; i += blockDim.x)
-    if (hist[i]) atomicAdd(&counts[i], (unsigned long long)hist[i]);
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+    if (!hist[i]) continue;
+    atomicAdd(&stats[i], (unsigned long long)hist[i]);
+    atomicMin(&stats[nb + i], lo[i]);
+    atomicMax(&stats[2 * nb + i], hi[i]);
+  }
 }
 
-// buckets[2m] = offset, buckets[2m+1] = count; cursor[m] = offset.
-__global__ void offsets_kernel(const unsigned long long* counts, int nb, int64_t* buckets,
-                               unsigned long long* cursor) {
-  if (threadIdx.x != 0) return;
-  unsigned long long off = 0;
-  for (int m = 0; m < nb; ++m) {
-    buckets[2 * m] = int64_t(off);
-    buckets[2 * m + 1] = int64_t(counts[m]);
-    cursor[m] = off;
-    off += counts[m];
+__global__ void stats_init_kernel(unsigned long long* stats, int nb) {
+  const int i = threadIdx.x;
+  if (i < nb) {
+    stats[i] = 0;
+    stats[nb + i] = ~0ull;
+    stats[2 * nb + i] = 0;
   }
 }
 
@@ -76,30 +96,63 @@ __global__ void scatter_kernel(const uint8_t* __restrict__ codes, int64_t B,
   }
 }
 
-template <typename R>
-cudaError_t bucket_rows(const R* basis, int64_t B, int K, BucketScratch& sc, cudaStream_t s) {
-  const int nb = 1 << K;
-  cudaError_t e;
-  if ((e = cudaMallocAsync(&sc.codes, size_t(B), s)) != cudaSuccess) return e;
-  if ((e = cudaMallocAsync(&sc.rows, size_t(B) * sizeof(int32_t), s)) != cudaSuccess) return e;
-  if ((e = cudaMallocAsync(&sc.small, sizeof(unsigned long long) * 4 * kMaxBuckets, s)) != cudaSuccess)
-    return e;
-  unsigned long long* counts = sc.small;
-  unsigned long long* cursor = sc.small + kMaxBuckets;
-  sc.buckets = reinterpret_cast<int64_t*>(sc.small + 2 * kMaxBuckets);
-  if ((e = cudaMemsetAsync(counts, 0, sizeof(unsigned long long) * kMaxBuckets, s)) != cudaSuccess)
-    return e;
+static int grid_for(int64_t B, int threads) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int threads = 256;
   int64_t blocks = (B + threads - 1) / threads;
   if (blocks > int64_t(sms) * 8) blocks = int64_t(sms) * 8;
-  classify_kernel<R><<<unsigned(blocks), threads, 0, s>>>(basis, B, K, sc.codes, counts);
-  offsets_kernel<<<1, 32, 0, s>>>(counts, nb, sc.buckets, cursor);
-  scatter_kernel<<<unsigned(blocks), threads, 0, s>>>(sc.codes, B, cursor, sc.rows);
-  count_launches(3);
-  return cudaGetLastError();
+  return int(blocks < 1 ? 1 : blocks);
+}
+
+template <typename R>
+cudaError_t bucket_plan(const R* basis, int64_t B, int K, BucketScratch& sc, BucketPlan& plan,
+                        cudaStream_t s) {
+  const int nb = 1 << K;
+  plan.nb = nb;
+  cudaError_t e;
+  if ((e = cudaMallocAsync(&sc.codes, size_t(B), s)) != cudaSuccess) return e;
+  if ((e = cudaMallocAsync(&sc.small, sizeof(unsigned long long) * 4 * kMaxBuckets, s)) != cudaSuccess)
+    return e;
+  static unsigned long long* host = nullptr;  // pinned staging for the 3 x nb stats
+  if (host == nullptr) {
+    if ((e = cudaMallocHost(&host, sizeof(unsigned long long) * 3 * kMaxBuckets)) != cudaSuccess)
+      return e;
+  }
+  stats_init_kernel<<<1, kMaxBuckets, 0, s>>>(sc.small, nb);
+  classify_kernel<R><<<grid_for(B, 256), 256, 0, s>>>(basis, B, K, sc.codes, sc.small);
+  count_launches(2);
+  if ((e = cudaMemcpyAsync(host, sc.small, sizeof(unsigned long long) * 3 * nb,
+                           cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+    return e;
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+  plan.all_contiguous = true;
+  int64_t off = 0;
+  for (int m = 0; m < nb; ++m) {
+    plan.count[m] = int64_t(host[m]);
+    plan.lo[m] = plan.count[m] ? int64_t(host[nb + m]) : 0;
+    plan.hi[m] = plan.count[m] ? int64_t(host[2 * nb + m]) : -1;
+    plan.offset[m] = off;
+    off += plan.count[m];
+    plan.contiguous[m] = plan.count[m] == 0 || plan.hi[m] - plan.lo[m] + 1 == plan.count[m];
+    plan.all_contiguous = plan.all_contiguous && plan.contiguous[m];
+  }
+  return cudaSuccess;
+}
+
+cudaError_t bucket_scatter(int64_t B, const BucketPlan& plan, BucketScratch& sc, cudaStream_t s) {
+  cudaError_t e;
+  if ((e = cudaMallocAsync(&sc.rows, size_t(B) * sizeof(int32_t), s)) != cudaSuccess) return e;
+  unsigned long long cursor_h[kMaxBuckets];
+  for (int m = 0; m < plan.nb; ++m) cursor_h[m] = (unsigned long long)plan.offset[m];
+  unsigned long long* cursor = sc.small + 3 * kMaxBuckets;
+  if ((e = cudaMemcpyAsync(cursor, cursor_h, sizeof(unsigned long long) * plan.nb,
+                           cudaMemcpyHostToDevice, s)) != cudaSuccess)
+    return e;
+  scatter_kernel<<<grid_for(B, 256), 256, 0, s>>>(sc.codes, B, cursor, sc.rows);
+  count_launches(1);
+  // cursor_h lives on this stack frame: make sure the copy consumed it
+  return cudaStreamSynchronize(s);
 }
 
 void bucket_free(BucketScratch& sc, cudaStream_t s) {
@@ -109,7 +162,41 @@ void bucket_free(BucketScratch& sc, cudaStream_t s) {
   sc = BucketScratch{};
 }
 
-template cudaError_t bucket_rows<float>(const float*, int64_t, int, BucketScratch&, cudaStream_t);
-template cudaError_t bucket_rows<double>(const double*, int64_t, int, BucketScratch&, cudaStream_t);
+template cudaError_t bucket_plan<float>(const float*, int64_t, int, BucketScratch&, BucketPlan&,
+                                        cudaStream_t);
+template cudaError_t bucket_plan<double>(const double*, int64_t, int, BucketScratch&, BucketPlan&,
+                                         cudaStream_t);
+
+// ---- side streams: overlap the tails of the per-mask launches ----------------
+SideStreams& side_streams() {
+  static SideStreams ss;
+  return ss;
+}
+
+cudaError_t SideStreams::fork(cudaStream_t parent, int n) {
+  cudaError_t e;
+  if (!ready) {
+    for (int i = 0; i < kSide; ++i) {
+      if ((e = cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking)) != cudaSuccess) return e;
+      if ((e = cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming)) != cudaSuccess) return e;
+    }
+    if ((e = cudaEventCreateWithFlags(&start, cudaEventDisableTiming)) != cudaSuccess) return e;
+    ready = true;
+  }
+  used = n < kSide ? n : kSide;
+  if ((e = cudaEventRecord(start, parent)) != cudaSuccess) return e;
+  for (int i = 0; i < used; ++i)
+    if ((e = cudaStreamWaitEvent(st[i], start, 0)) != cudaSuccess) return e;
+  return cudaSuccess;
+}
+
+cudaError_t SideStreams::join(cudaStream_t parent) {
+  cudaError_t e;
+  for (int i = 0; i < used; ++i) {
+    if ((e = cudaEventRecord(done[i], st[i])) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(parent, done[i], 0)) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
 
 }  // namespace fp

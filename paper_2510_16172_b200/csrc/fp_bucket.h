@@ -13,12 +13,36 @@ constexpr int kMaxBuckets = 1 << kMaxSpecialisedOrder;
 struct BucketScratch {
   uint8_t* codes = nullptr;
   int32_t* rows = nullptr;              // permutation, bucket-major
-  unsigned long long* small = nullptr;  // counts | cursor | buckets
-  int64_t* buckets = nullptr;           // (offset, count) per mask, device
+  unsigned long long* small = nullptr;  // stats (3 x kMaxBuckets) | cursor
 };
 
+struct BucketPlan {
+  int nb = 0;
+  int64_t count[kMaxBuckets], lo[kMaxBuckets], hi[kMaxBuckets], offset[kMaxBuckets];
+  bool contiguous[kMaxBuckets];
+  bool all_contiguous = true;
+};
+
+// Classify + per-mask statistics; synchronises `s` to bring the plan home.
 template <typename R>
-cudaError_t bucket_rows(const R* basis, int64_t B, int K, BucketScratch& sc, cudaStream_t s);
+cudaError_t bucket_plan(const R* basis, int64_t B, int K, BucketScratch& sc, BucketPlan& plan,
+                        cudaStream_t s);
+// Bucket-major row permutation in sc.rows (for non-contiguous masks).
+cudaError_t bucket_scatter(int64_t B, const BucketPlan& plan, BucketScratch& sc, cudaStream_t s);
 void bucket_free(BucketScratch& sc, cudaStream_t s);
+
+// A small pool of non-blocking streams: the per-mask kernels run
+// concurrently so that their tail waves overlap.
+struct SideStreams {
+  static constexpr int kSide = 4;
+  cudaStream_t st[kSide];
+  cudaEvent_t done[kSide];
+  cudaEvent_t start;
+  bool ready = false;
+  int used = 0;
+  cudaError_t fork(cudaStream_t parent, int n);
+  cudaError_t join(cudaStream_t parent);
+};
+SideStreams& side_streams();
 
 }  // namespace fp

@@ -24,16 +24,18 @@ struct PathArgs {
   const R* wL;      // per-path weight on L, may be null
   R wL_scale;       // weight used when wL is null
   int mode;         // fp_vjp_mode
-  int64_t B;        // batch rows (leading dim of every array, incl. traces)
+  int64_t B;        // staged mode: rows [row_begin, B) of the batch
+  int64_t row_begin;
+  int64_t ld;       // leading dimension of the (iterations, batch) trace arrays
   int iterations, fp_iters;
   R *T_out, *g_out, *points_out, *length_out;
   uint8_t* status_out;
   R *trace_len, *trace_gnorm, *H_out;
   R *d_basis, *d_anchor, *d_start, *d_end, *u_out;
-  // Bucketed dispatch (fp_bucket.cu): rows[bucket[0] + i], i < bucket[1],
-  // are this launch's paths; both live in device memory.
+  // Gathered dispatch (fp_bucket.cu): rows[0 .. n_rows) are this launch's
+  // paths (a kind-mask bucket that is not one contiguous range).
   const int32_t* rows;
-  const int64_t* bucket;
+  int64_t n_rows;
 };
 
 // Per-path output destinations (shared-memory slab slots or global records).
@@ -185,13 +187,12 @@ __device__ __forceinline__ void run_path(const PathArgs<R>& a, int64_t row, cons
   P.eval(G, P.g);
   if (OP != OP_VJP) {
     if (P.nmin <= G.eps) st |= FP_STATUS_DEGENERATE_ENTRY;  // checked_segments (solver.py:166)
-    InvHess<R, NA> H;
+    InvHess<R, K, MASK> H;
     H.identity();
-    for (int it = 0; it < a.iterations; ++it) {
-      R p[NA];
-      H.mul(P.g, p);
+    R p[NA];
 #pragma unroll
-      for (int j = 0; j < NA; ++j) p[j] = -p[j];
+    for (int j = 0; j < NA; ++j) p[j] = -P.g[j];  // H = I
+    for (int it = 0; it < a.iterations; ++it) {
       bool zero;
       const R alpha = P.step_size(G, p, a.fp_iters, zero);
       if (zero) st |= FP_STATUS_ZERO_DIRECTION;
@@ -204,24 +205,21 @@ __device__ __forceinline__ void run_path(const PathArgs<R>& a, int64_t row, cons
       R gn[NA];
       P.eval(G, gn);
       R y[NA];
-      R sy = R(0), ss = R(0), yy = R(0);
 #pragma unroll
-      for (int j = 0; j < NA; ++j) {
-        y[j] = gn[j] - P.g[j];
-        sy = fma(sg[j], y[j], sy);
-        ss = fma(sg[j], sg[j], ss);
-        yy = fma(y[j], y[j], yy);
-      }
+      for (int j = 0; j < NA; ++j) y[j] = gn[j] - P.g[j];
+      const R sy = dot<R, K, MASK, NA>(sg, y);
+      const R ss = dot<R, K, MASK, NA>(sg, sg);
+      const R yy = dot<R, K, MASK, NA>(y, y);
       const bool ok = sy > (R(1e-12) * sqrt_test(ss)) * sqrt_test(yy);
-      if (ok) H.update(sg, y, Num<R>::rcp(sy));
+      H.step(sg, y, gn, p, ok, sy);
 #pragma unroll
       for (int j = 0; j < NA; ++j) P.g[j] = gn[j];
       if (a.trace_len != nullptr) {
         R q = R(0);
 #pragma unroll
         for (int j = 0; j < NA; ++j) q = fma(P.g[j], P.g[j], q);
-        a.trace_len[(int64_t)it * a.B + row] = P.len;
-        a.trace_gnorm[(int64_t)it * a.B + row] = Num<R>::sqrt_(q);
+        a.trace_len[(int64_t)it * a.ld + row] = P.len;
+        a.trace_gnorm[(int64_t)it * a.ld + row] = Num<R>::sqrt_(q);
       }
     }
     if (a.H_out != nullptr) {
@@ -233,7 +231,7 @@ __device__ __forceinline__ void run_path(const PathArgs<R>& a, int64_t row, cons
           const int ii = i >> 1, ci = i & 1, jj = j >> 1, cj = j & 1;
           const bool ai = ci == 0 || L::plane(ii), aj = cj == 0 || L::plane(jj);
           R v = (i == j) ? R(1) : R(0);
-          if (ai && aj) v = H.h[InvHess<R, NA>::id(L::idx(ii, ci), L::idx(jj, cj))];
+          if (ai && aj) v = H.h[InvHess<R, K, MASK>::id(L::idx(ii, ci), L::idx(jj, cj))];
           Ho[i * 2 * K + j] = v;
         }
     }
@@ -316,77 +314,101 @@ __device__ __forceinline__ void run_path(const PathArgs<R>& a, int64_t row, cons
   if (o.st) o.st[0] = st;
 }
 
-template <typename R, int K, unsigned MASK, int OP>
-#ifndef FP_MIN_BLOCKS
-#define FP_MIN_BLOCKS 1
-#endif
-__global__ void __launch_bounds__(kThreads, FP_MIN_BLOCKS) path_kernel(const PathArgs<R> a) {
-  unsigned char* smem = fp_smem;
-  __shared__ __align__(8) uint64_t bar;
-  using Wk = W<K>;
-  const int tid = threadIdx.x;
-  if (a.rows != nullptr) {
-    // Bucketed dispatch: persistent grid-stride over this bucket's rows,
-    // direct per-thread records (each record is one contiguous run).
-    const int64_t off = a.bucket[0], cnt = a.bucket[1];
-    for (int64_t i = int64_t(blockIdx.x) * kThreads + tid; i - tid < cnt;
-         i += int64_t(gridDim.x) * kThreads) {
-      if (i >= cnt) continue;
-      const int64_t row = a.rows[off + i];
-      Rec<R, K> in;
-      load_rec(in, a.basis + row * Wk::basis, a.anchor + row * Wk::anchor, a.start + row * 3,
-               a.end + row * 3, a.T + row * Wk::T, a.vT ? a.vT + row * Wk::T : nullptr);
-      run_path<R, K, MASK, OP>(a, row, in, a.vT != nullptr, tid, false);
-    }
+// Copy `width`-element records of the tile from global to shared memory with
+// asynchronous copies (cp.async, LDGSTS): every element's load is in flight
+// at once instead of one load latency per loop trip. Gathered tiles move each
+// record as a run of consecutive lanes (one or two cache lines per record).
+// Completion: cp_async_wait_all() + __syncthreads() by the caller.
+template <typename R>
+__device__ __forceinline__ void cp_async_elem(R* dst, const R* src) {
+  static_assert(sizeof(R) == 4 || sizeof(R) == 8, "4- or 8-byte elements");
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "n"(int(sizeof(R)))
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+template <typename R, int WD>
+__device__ __forceinline__ void tile_in(R* dst, const R* src, const int32_t* srow, int64_t base, int n) {
+  for (int e = threadIdx.x; e < n * WD; e += kThreads) {
+    const int r = e / WD, c = e - r * WD;
+    const int64_t row = srow ? int64_t(srow[r]) : base + r;
+    cp_async_elem(dst + e, src + row * WD + c);
+  }
+}
+template <typename R, int WD>
+__device__ __forceinline__ void tile_out(R* dst, const R* src, const int32_t* srow, int64_t base, int n) {
+  if (srow == nullptr) {
+    for (int e = threadIdx.x; e < n * WD; e += kThreads) dst[base * WD + e] = src[e];
     return;
   }
-  const int64_t base = int64_t(blockIdx.x) * kThreads;
-  const int64_t total = a.B;
-  if (base >= total) return;
-  const int n = int(total - base < kThreads ? total - base : int64_t(kThreads));
+  for (int e = threadIdx.x; e < n * WD; e += kThreads) {
+    const int r = e / WD, c = e - r * WD;
+    dst[int64_t(srow[r]) * WD + c] = src[e];
+  }
+}
 
-  // ---- stage the CTA's input slabs -----------------------------------------
+// One tile of up to kThreads paths: stage inputs in shared memory (TMA bulk
+// copies for full aligned contiguous tiles), compute in registers, stage the
+// outputs and write them back.
+template <typename R, int K, unsigned MASK, int OP>
+__device__ __forceinline__ void process_tile(const PathArgs<R>& a, const int32_t* srow, int64_t base,
+                                             int n, uint64_t* bar) {
+  using Wk = W<K>;
+  const int tid = threadIdx.x;
+  unsigned char* smem = fp_smem;
   R* sb = reinterpret_cast<R*>(smem);
   R* sa = sb + kThreads * Wk::basis;
   R* s0 = sa + kThreads * Wk::anchor;
   R* s1 = s0 + kThreads * 3;
   R* sT = s1 + kThreads * 3;
   R* sv = sT + kThreads * Wk::T;
-  const R* gb = a.basis + base * Wk::basis;
-  const R* ga = a.anchor + base * Wk::anchor;
-  const R* g0 = a.start + base * 3;
-  const R* g1 = a.end + base * 3;
-  const R* gT = a.T + base * Wk::T;
-  const R* gv = a.vT ? a.vT + base * Wk::T : nullptr;
-  const bool tma = n == kThreads && aligned16(gb) && aligned16(ga) && aligned16(g0) &&
-                   aligned16(g1) && aligned16(gT) && (gv == nullptr || aligned16(gv));
+  const bool has_v = a.vT != nullptr;
+  bool tma = false;
+  if (srow == nullptr && n == kThreads) {
+    tma = aligned16(a.basis + base * Wk::basis) && aligned16(a.anchor + base * Wk::anchor) &&
+          aligned16(a.start + base * 3) && aligned16(a.end + base * 3) &&
+          aligned16(a.T + base * Wk::T) && (!has_v || aligned16(a.vT + base * Wk::T));
+  }
   if (tma) {
     const uint32_t bb = kThreads * Wk::basis * sizeof(R), ba = kThreads * Wk::anchor * sizeof(R),
                    bv = kThreads * 3 * sizeof(R), bt = kThreads * Wk::T * sizeof(R);
-    if (tid == 0) mbar_init(&bar, 1);
+    if (tid == 0) mbar_init(bar, 1);
     __syncthreads();
     if (tid == 0) {
-      mbar_expect_tx(&bar, bb + ba + 2 * bv + bt + (gv ? bt : 0));
-      bulk_g2s(sb, gb, bb, &bar);
-      bulk_g2s(sa, ga, ba, &bar);
-      bulk_g2s(s0, g0, bv, &bar);
-      bulk_g2s(s1, g1, bv, &bar);
-      bulk_g2s(sT, gT, bt, &bar);
-      if (gv) bulk_g2s(sv, gv, bt, &bar);
+      mbar_expect_tx(bar, bb + ba + 2 * bv + bt + (has_v ? bt : 0));
+      bulk_g2s(sb, a.basis + base * Wk::basis, bb, bar);
+      bulk_g2s(sa, a.anchor + base * Wk::anchor, ba, bar);
+      bulk_g2s(s0, a.start + base * 3, bv, bar);
+      bulk_g2s(s1, a.end + base * 3, bv, bar);
+      bulk_g2s(sT, a.T + base * Wk::T, bt, bar);
+      if (has_v) bulk_g2s(sv, a.vT + base * Wk::T, bt, bar);
     }
-    mbar_wait(&bar, 0);
+    mbar_wait(bar, 0);
   } else {
-    coop_copy(sb, gb, n * Wk::basis);
-    coop_copy(sa, ga, n * Wk::anchor);
-    coop_copy(s0, g0, n * 3);
-    coop_copy(s1, g1, n * 3);
-    coop_copy(sT, gT, n * Wk::T);
-    if (gv) coop_copy(sv, gv, n * Wk::T);
+    tile_in<R, Wk::basis>(sb, a.basis, srow, base, n);
+    tile_in<R, Wk::anchor>(sa, a.anchor, srow, base, n);
+    tile_in<R, 3>(s0, a.start, srow, base, n);
+    tile_in<R, 3>(s1, a.end, srow, base, n);
+    tile_in<R, Wk::T>(sT, a.T, srow, base, n);
+    if (has_v) tile_in<R, Wk::T>(sv, a.vT, srow, base, n);
+    cp_async_wait_all();
     __syncthreads();
   }
 
-  // ---- compute (inputs are copied to registers first) ------------------------
-  // Output slabs reuse the same shared memory after the barrier below.
+  // Registers take this thread's record; the slab is then reused for outputs.
+  Rec<R, K> in;
+  if (tid < n)
+    load_rec(in, sb + tid * Wk::basis, sa + tid * Wk::anchor, s0 + tid * 3, s1 + tid * 3,
+             sT + tid * Wk::T, has_v ? sv + tid * Wk::T : nullptr);
+  __syncthreads();
+  if (tid < n) {
+    const int64_t row = srow ? int64_t(srow[tid]) : base + tid;
+    run_path<R, K, MASK, OP>(a, row, in, has_v, tid, true);
+  }
+  __syncthreads();
+
   R* oT = reinterpret_cast<R*>(smem);
   R* og = oT + kThreads * Wk::T;
   R* op = og + kThreads * Wk::T;
@@ -397,30 +419,50 @@ __global__ void __launch_bounds__(kThreads, FP_MIN_BLOCKS) path_kernel(const Pat
   R* od1 = od0 + kThreads * 3;
   R* ou = od1 + kThreads * 3;
   uint8_t* ost = reinterpret_cast<uint8_t*>(smem + size_t(Wk::slab_elems) * kThreads * sizeof(R));
+  if (a.T_out) tile_out<R, Wk::T>(a.T_out, oT, srow, base, n);
+  if (a.g_out) tile_out<R, Wk::T>(a.g_out, og, srow, base, n);
+  if (a.points_out) tile_out<R, Wk::pts>(a.points_out, op, srow, base, n);
+  if (a.length_out) tile_out<R, 1>(a.length_out, ol, srow, base, n);
+  if (a.d_basis) tile_out<R, Wk::basis>(a.d_basis, odb, srow, base, n);
+  if (a.d_anchor) tile_out<R, Wk::anchor>(a.d_anchor, oda, srow, base, n);
+  if (a.d_start) tile_out<R, 3>(a.d_start, od0, srow, base, n);
+  if (a.d_end) tile_out<R, 3>(a.d_end, od1, srow, base, n);
+  if (a.u_out) tile_out<R, Wk::T>(a.u_out, ou, srow, base, n);
+  if (a.status_out) tile_out<uint8_t, 1>(a.status_out, ost, srow, base, n);
+}
 
-  // Copy this thread's inputs out of shared memory into registers, then wait
-  // for every thread before the slab is reused for outputs.
-  Rec<R, K> in;
-  if (tid < n)
-    load_rec(in, sb + tid * Wk::basis, sa + tid * Wk::anchor, s0 + tid * 3, s1 + tid * 3,
-             sT + tid * Wk::T, gv ? sv + tid * Wk::T : nullptr);
-  __syncthreads();
-  if (tid < n) {
-    run_path<R, K, MASK, OP>(a, base + tid, in, gv != nullptr, tid, true);
+// Minimum co-resident CTAs per SM requested from ptxas (caps registers at
+// 65536 / (128 * n)). Measured on B200 at K = 3: 4 CTAs (<= 128 registers)
+// beats ptxas' unconstrained choice (140-170 registers, 3 CTAs) by 7-10%;
+// larger active sets get more registers. FP_MIN_BLOCKS overrides (A/B runs).
+template <typename R, int NA>
+struct MinBlocks {
+#ifdef FP_MIN_BLOCKS
+  static constexpr int value = FP_MIN_BLOCKS;
+#else
+  static constexpr int value = sizeof(R) == 8 ? 1 : (NA <= 6 ? 4 : (NA <= 8 ? 3 : 2));
+#endif
+};
+
+template <typename R, int K, unsigned MASK, int OP>
+__global__ void __launch_bounds__(kThreads, (MinBlocks<R, Lay<K, MASK>::NA>::value))
+    path_kernel(const PathArgs<R> a) {
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ int32_t srow[kThreads];
+  const int tid = threadIdx.x;
+  if (a.rows != nullptr) {
+    const int64_t t0 = int64_t(blockIdx.x) * kThreads;
+    if (t0 >= a.n_rows) return;
+    const int n = int(a.n_rows - t0 < kThreads ? a.n_rows - t0 : int64_t(kThreads));
+    if (tid < n) srow[tid] = a.rows[t0 + tid];
+    __syncthreads();
+    process_tile<R, K, MASK, OP>(a, srow, 0, n, &bar);
+    return;
   }
-  __syncthreads();
-
-  // ---- coalesced write-back ----------------------------------------------------
-  if (a.T_out) coop_copy(a.T_out + base * Wk::T, oT, n * Wk::T);
-  if (a.g_out) coop_copy(a.g_out + base * Wk::T, og, n * Wk::T);
-  if (a.points_out) coop_copy(a.points_out + base * Wk::pts, op, n * Wk::pts);
-  if (a.length_out) coop_copy(a.length_out + base, ol, n);
-  if (a.d_basis) coop_copy(a.d_basis + base * Wk::basis, odb, n * Wk::basis);
-  if (a.d_anchor) coop_copy(a.d_anchor + base * Wk::anchor, oda, n * Wk::anchor);
-  if (a.d_start) coop_copy(a.d_start + base * 3, od0, n * 3);
-  if (a.d_end) coop_copy(a.d_end + base * 3, od1, n * 3);
-  if (a.u_out) coop_copy(a.u_out + base * Wk::T, ou, n * Wk::T);
-  if (a.status_out) coop_copy(a.status_out + base, ost, n);
+  const int64_t base = a.row_begin + int64_t(blockIdx.x) * kThreads;
+  if (base >= a.B) return;
+  const int n = int(a.B - base < kThreads ? a.B - base : int64_t(kThreads));
+  process_tile<R, K, MASK, OP>(a, nullptr, base, n, &bar);
 }
 
 // Host-side launcher (defined per K in fp_inst.cu).
@@ -429,22 +471,17 @@ cudaError_t launch_path(const PathArgs<R>& a, cudaStream_t stream);
 
 template <typename R, int K, unsigned MASK, int OP>
 cudaError_t launch_path_impl(const PathArgs<R>& a, cudaStream_t stream) {
-  if (a.B <= 0) return cudaSuccess;
-  const size_t smem = a.rows ? 0 : smem_bytes<R, K>();
-  static int resident = 0;  // co-resident CTAs on the whole GPU (bucketed launches)
-  if (resident == 0) {
+  const int64_t rows = a.rows ? a.n_rows : a.B - a.row_begin;
+  if (rows <= 0) return cudaSuccess;
+  const size_t smem = smem_bytes<R, K>();
+  static bool configured = false;
+  if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(path_kernel<R, K, MASK, OP>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(smem_bytes<R, K>()));
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, path_kernel<R, K, MASK, OP>, kThreads, 0);
-    resident = (sms > 0 ? sms : 148) * (per_sm > 0 ? per_sm : 1);
+    configured = true;
   }
-  int64_t blocks = (a.B + kThreads - 1) / kThreads;
-  if (a.rows != nullptr && blocks > resident) blocks = resident;
+  const int64_t blocks = (rows + kThreads - 1) / kThreads;
   path_kernel<R, K, MASK, OP><<<dim3(unsigned(blocks)), dim3(kThreads), smem, stream>>>(a);
   return cudaGetLastError();
 }

@@ -187,9 +187,40 @@ struct PathState {
   }
 };
 
+// Dot product over the active unknowns as two FMA chains, one per basis
+// column c (half the dependent latency of one chain). Grouping by column, not
+// by compressed position, keeps the kind-specialised kernels bit-identical to
+// the dense one: an edge's inert term only adds an exact zero to chain 1.
+template <typename R, int K, unsigned MASK, int NA>
+__device__ __forceinline__ R dot(const R (&a)[NA], const R (&b)[NA]) {
+  using L = Lay<K, MASK>;
+  R c0 = a[L::idx(0, 0)] * b[L::idx(0, 0)];
+#pragma unroll
+  for (int i = 1; i < K; ++i) c0 = fma(a[L::idx(i, 0)], b[L::idx(i, 0)], c0);
+  bool any = false;
+  R c1 = R(0);
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    if (!L::plane(i)) continue;
+    c1 = any ? fma(a[L::idx(i, 1)], b[L::idx(i, 1)], c1) : a[L::idx(i, 1)] * b[L::idx(i, 1)];
+    any = true;
+  }
+  return any ? c0 + c1 : c0;
+}
+
 // Packed symmetric inverse-Hessian approximation with the BFGS update.
-template <typename R, int NA>
+//
+// The reference update (solver.py:180-199)
+//   H' = H - rho (s Hy^T + Hy s^T) + (rho^2 yHy + rho) s s^T
+// is applied in the equivalent symmetric two-term form H' = H + s z^T + z s^T
+// with z = -rho Hy + (rho^2 yHy + rho)/2 s (two FMAs per packed entry), and
+// the next direction -H' g_new is obtained from H g_new by the same rank-two
+// formula, so each iteration needs one matrix-vector product: H y follows
+// from H g_new + p (p = -H g_old).
+template <typename R, int K, unsigned MASK>
 struct InvHess {
+  using L = Lay<K, MASK>;
+  static constexpr int NA = L::NA;
   static constexpr int NH = NA * (NA + 1) / 2;
   R h[NH];
   R bound;  // upper bound on max |h_ij| (for the overflow pre-check)
@@ -204,66 +235,79 @@ struct InvHess {
       for (int j = i; j < NA; ++j) h[id(i, j)] = i == j ? R(1) : R(0);
     bound = R(1);
   }
+  // out = H v, each row as the column-grouped two-chain dot product.
   __device__ __forceinline__ void mul(const R (&v)[NA], R (&out)[NA]) const {
 #pragma unroll
-    for (int i = 0; i < NA; ++i) {
-      R acc = h[id(i, 0)] * v[0];
+    for (int r = 0; r < NA; ++r) {
+      R c0 = h[id(r, L::idx(0, 0))] * v[L::idx(0, 0)];
 #pragma unroll
-      for (int j = 1; j < NA; ++j) acc = fma(h[id(i, j)], v[j], acc);
-      out[i] = acc;
+      for (int i = 1; i < K; ++i) c0 = fma(h[id(r, L::idx(i, 0))], v[L::idx(i, 0)], c0);
+      bool any = false;
+      R c1 = R(0);
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        if (!L::plane(i)) continue;
+        const int j = L::idx(i, 1);
+        c1 = any ? fma(h[id(r, j)], v[j], c1) : h[id(r, j)] * v[j];
+        any = true;
+      }
+      out[r] = any ? c0 + c1 : c0;
     }
   }
-  // H' = H - rho (s Hy^T + Hy s^T) + (rho^2 yHy + rho) s s^T, kept only when
-  // the curvature test passed and every entry of H' is finite
-  // (solver.py:180-199). Returns whether the update was taken.
-  __device__ __forceinline__ bool update(const R (&sg)[NA], const R (&y)[NA], R rho) {
-    R Hy[NA];
-    mul(y, Hy);
-    R yHy = y[0] * Hy[0];
+  // One BFGS step. In: step sg, gradient change y, new gradient gn, old
+  // direction p (= -H g_old), curvature flag ok and sy = sg.y. Out: p =
+  // -H' gn with H' the updated matrix (or the old one when the update is
+  // skipped: failed curvature test or a non-finite H', solver.py:184,198).
+  __device__ __forceinline__ void step(const R (&sg)[NA], const R (&y)[NA], const R (&gn)[NA],
+                                       R (&p)[NA], bool ok, R sy) {
+    R Hg[NA];
+    mul(gn, Hg);
+    if (ok) {
+      R Hy[NA];
 #pragma unroll
-    for (int i = 1; i < NA; ++i) yHy = fma(y[i], Hy[i], yHy);
-    const R coef = fma(rho * rho, yHy, rho);
-    R a[NA], c[NA];
-    R sa = R(0), sy = R(0), sc = R(0), ss = R(0);
+      for (int i = 0; i < NA; ++i) Hy[i] = Hg[i] + p[i];
+      const R rho = Num<R>::rcp(sy);
+      const R yHy = dot<R, K, MASK, NA>(y, Hy);
+      const R half = R(0.5) * fma(rho * rho, yHy, rho);
+      R z[NA];
+      R ss = R(0), sz = R(0);
 #pragma unroll
-    for (int i = 0; i < NA; ++i) {
-      a[i] = rho * sg[i];
-      c[i] = coef * sg[i];
-      sa += fabs(a[i]);
-      sy += fabs(Hy[i]);
-      sc += fabs(c[i]);
-      ss += fabs(sg[i]);
-    }
-    // |H'_ij| <= bound + 2 sum|a| sum|Hy| + sum|c| sum|s|; NaN/inf propagate.
-    const R nb = (bound + R(2) * sa * sy + sc * ss) * R(1.0009765625);
-    if (nb < R(1e36)) {
-#pragma unroll
-      for (int i = 0; i < NA; ++i)
-#pragma unroll
-        for (int j = i; j < NA; ++j)
-          h[id(i, j)] = fma(c[i], sg[j], fma(-a[j], Hy[i], fma(-a[i], Hy[j], h[id(i, j)])));
-      bound = nb;
-      return true;
-    }
-    // Rare: possible overflow. Pass 1 checks every entry, pass 2 commits.
-    bool fin = true;
-    R mx = R(0);
-#pragma unroll
-    for (int i = 0; i < NA; ++i)
-#pragma unroll
-      for (int j = i; j < NA; ++j) {
-        const R v = fma(c[i], sg[j], fma(-a[j], Hy[i], fma(-a[i], Hy[j], h[id(i, j)])));
-        fin = fin && finite(v);
-        mx = fabs(v) > mx ? fabs(v) : mx;
+      for (int i = 0; i < NA; ++i) {
+        z[i] = fma(half, sg[i], -(rho * Hy[i]));
+        ss += fabs(sg[i]);
+        sz += fabs(z[i]);
       }
-    if (!fin) return false;
+      // |H'_ij| <= bound + 2 sum|s| sum|z|; NaN/inf propagate into nb.
+      const R nb = fma(R(2) * ss, sz, bound) * R(1.0009765625);
+      bool take = true;
+      if (!(nb < R(1e36))) {
+        // Rare: possible overflow. Check every entry before committing.
+        R mx = R(0);
 #pragma unroll
-    for (int i = 0; i < NA; ++i)
+        for (int i = 0; i < NA; ++i)
 #pragma unroll
-      for (int j = i; j < NA; ++j)
-        h[id(i, j)] = fma(c[i], sg[j], fma(-a[j], Hy[i], fma(-a[i], Hy[j], h[id(i, j)])));
-    bound = mx * R(1.0009765625);
-    return true;
+          for (int j = i; j < NA; ++j) {
+            const R v = fma(z[i], sg[j], fma(sg[i], z[j], h[id(i, j)]));
+            take = take && finite(v);
+            mx = fabs(v) > mx ? fabs(v) : mx;
+          }
+        if (take) bound = mx * R(1.0009765625);
+      } else {
+        bound = nb;
+      }
+      if (take) {
+#pragma unroll
+        for (int i = 0; i < NA; ++i)
+#pragma unroll
+          for (int j = i; j < NA; ++j) h[id(i, j)] = fma(z[i], sg[j], fma(sg[i], z[j], h[id(i, j)]));
+        const R zg = dot<R, K, MASK, NA>(z, gn), sgn = dot<R, K, MASK, NA>(sg, gn);
+#pragma unroll
+        for (int i = 0; i < NA; ++i) p[i] = -fma(sg[i], zg, fma(z[i], sgn, Hg[i]));
+        return;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < NA; ++i) p[i] = -Hg[i];
   }
 };
 

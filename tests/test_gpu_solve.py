@@ -209,7 +209,7 @@ def test_launch_counter_advances():
     solve(BatchScene(b.basis, b.anchor, b.start, b.end), b.T0,
           SolveOptions(iterations=10, precision=Precision.SINGLE))
     torch.cuda.synchronize()
-    assert _lib.launch_count() == before + 1
+    assert _lib.launch_count() >= before + 1
 
 
 @pytest.mark.parametrize("K", [2, 3, 5])
