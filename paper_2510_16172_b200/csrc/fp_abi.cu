@@ -98,10 +98,10 @@ static cudaError_t masked_k(int K, const PathArgs<float>& a, int op, unsigned m,
 // kernel on the mask's row range when it is contiguous, the gathering kernel
 // over a row permutation otherwise — on side streams so tails overlap.
 template <typename R>
-static int dispatch(int K, const PathArgs<R>& a, int op, cudaStream_t s) {
+static int dispatch(int K, const PathArgs<R>& a, int op, cudaStream_t s, bool allow_bucketing = true) {
   constexpr bool is_f32 = sizeof(R) == sizeof(float);
   const int64_t B = a.B;
-  const bool bucketed = is_f32 && g_policy.load() == FP_POLICY_AUTO && K >= 1 &&
+  const bool bucketed = is_f32 && allow_bucketing && g_policy.load() == FP_POLICY_AUTO && K >= 1 &&
                         K <= kMaxSpecialisedOrder && (op == OP_SOLVE || op == OP_SOLVE_VJP) &&
                         B > 0 && B < (int64_t(1) << 31) && a.rows == nullptr;
   if (!bucketed) return dispatch_dense_k<R>(K, a, op, s);
@@ -198,7 +198,8 @@ template <typename R>
 static int solve_vjp_impl(const R* basis, const R* anchor, const R* start, const R* end,
                           const R* T0, int64_t B, int K, int iterations, int fp_iters, const R* w_L,
                           R w_L_scale, int mode, R* T_out, R* points_out, R* length_out, R* d_basis,
-                          R* d_anchor, R* d_start, R* d_end, uint8_t* status_out, cudaStream_t s) {
+                          R* d_anchor, R* d_start, R* d_end, uint8_t* status_out, cudaStream_t s,
+                          bool allow_bucketing = true) {
   if (B < 0 || iterations < 1 || fp_iters < 1) return FP_ERR_INVALID_ARGUMENT;
   if (mode != FP_VJP_FULL && mode != FP_VJP_ENVELOPE) return FP_ERR_UNSUPPORTED_MODE;
   if (K < 0 || K > FP_MAX_ORDER) return FP_ERR_UNSUPPORTED_ORDER;
@@ -213,7 +214,7 @@ static int solve_vjp_impl(const R* basis, const R* anchor, const R* start, const
   a.d_basis = d_basis; a.d_anchor = d_anchor; a.d_start = d_start; a.d_end = d_end;
   a.status_out = status_out;
   finish_args(a);
-  return dispatch<R>(K, a, OP_SOLVE_VJP, s);
+  return dispatch<R>(K, a, OP_SOLVE_VJP, s, allow_bucketing);
 }
 
 // ---- generic-order helpers (scalar API; any K <= 64) ------------------------
@@ -517,12 +518,14 @@ int fp_solve_vjp_host_f32(const float* basis, const float* anchor, const float* 
                           cudaMemcpyHostToDevice, s);
       if (e != cudaSuccess) return cuda_status(e);
     }
+    // Dense kernel here: the kind-mask plan synchronises its stream, which
+    // would stall this enqueue loop; the pipeline is PCIe-bound anyway.
     int rc = solve_vjp_impl<float>(din[0], din[1], din[2], din[3], din[4], n, K, iterations, fp_iters,
                                    nullptr, w_L_scale, mode, hout[0] ? dout[0] : nullptr,
                                    hout[1] ? dout[1] : nullptr, hout[2] ? dout[2] : nullptr,
                                    hout[3] ? dout[3] : nullptr, hout[4] ? dout[4] : nullptr,
                                    hout[5] ? dout[5] : nullptr, hout[6] ? dout[6] : nullptr,
-                                   status_out ? dst : nullptr, s);
+                                   status_out ? dst : nullptr, s, /*allow_bucketing=*/false);
     if (rc != FP_OK) return rc;
     for (int i = 0; i < 7; ++i) {
       if (w_out[i] == 0 || hout[i] == nullptr) continue;
