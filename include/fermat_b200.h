@@ -136,6 +136,36 @@ int fp_line_search_f64(const double* basis, const double* anchor, const double* 
 int fp_init_params_f64(const double* basis, const double* anchor, const double* start,
                        const double* end, int64_t B, int K, double* T_out, void* stream);
 
+/* ---- candidate enumeration + tracing (BASELINE configs 3 and 4) -----------
+ * No reference code exists; the specification is in
+ * csrc/fp_enum.cu and DESIGN.md. Objects: obj_basis (N,3,2), obj_anchor
+ * (N,3); plane_ids / edge_ids list the reflector and edge objects. One call
+ * covers candidates [cand_begin, cand_end) of one (order <= 3, kind pattern)
+ * group, RX-major: candidate c -> rx = c / count_p, sequence c % count_p.
+ * Per-RX sequence count of a pattern (host function; -1 if invalid): */
+int64_t fp_enum_pattern_count(int n_planes, int n_edges, int order, unsigned pattern);
+/* Decode candidates to (rx, object sequence) — the enumeration itself. */
+int fp_enum_decode(const int32_t* plane_ids, int n_planes, const int32_t* edge_ids, int n_edges,
+                   int n_rx, int order, unsigned pattern, int64_t cand_begin, int64_t cand_end,
+                   int32_t* rx_out, int32_t* seq_out, void* stream);
+/* Fused decode -> solve (zero init) -> bounds mask -> compaction of VALID
+ * paths (converged and inside every object). counters (device, 4 x u64,
+ * accumulated): candidates, converged, in-bounds, valid (= records written
+ * when below `capacity`). With obj_grad (N,9: basis 6 + anchor 3) non-NULL,
+ * also accumulates loss += sum 1/L^2 and the gradients of that loss (full
+ * implicit VJP, cotangent -2/L^3) into obj_grad, tx_grad (3), rx_grad (n_rx,3). */
+int fp_enum_trace_f32(const float* obj_basis, const float* obj_anchor, const int32_t* plane_ids,
+                      int n_planes, const int32_t* edge_ids, int n_edges, const float* tx,
+                      const float* rx, int n_rx, int order, unsigned pattern, int64_t cand_begin,
+                      int64_t cand_end, int iterations, int fp_iters,
+                      unsigned long long* counters, int64_t capacity, int32_t* rec_rx,
+                      int32_t* rec_seq, float* rec_T, float* rec_L, float* rec_points,
+                      float* obj_grad, float* tx_grad, float* rx_grad, float* loss, void* stream);
+/* Object-parameter gradients -> vertex gradients: vert_ids (N,4) (-1 unused),
+ * coef (N,3,4) for (anchor, basis col 0, basis col 1) x vertex slot. */
+int fp_vertex_chain_f32(const float* obj_grad, int n_objects, const int32_t* vert_ids,
+                        const float* coef, float* vertex_grad, void* stream);
+
 /* ---- FP32 roofline probe ----------------------------------------------------
  * blocks x 256 threads, each running iters x 128 dependent-free FFMAs; the
  * bench times it with CUDA events to measure the FP32 SIMT peak. */

@@ -66,13 +66,19 @@ _SIGS = {
     "fp_line_search_f64": [_P] * 7 + [_I64, _I, _I] + [_P] * 2 + [_P],
     "fp_init_params_f64": [_P] * 4 + [_I64, _I, _P, _P],
     "fp_peak_ffma": [_I, _I, _P, _P],
+    "fp_enum_pattern_count": [_I, _I, _I, C.c_uint],
+    "fp_enum_decode": [_P, _I, _P, _I, _I, _I, C.c_uint, _I64, _I64, _P, _P, _P],
+    "fp_enum_trace_f32": [_P, _P, _P, _I, _P, _I, _P, _P, _I, _I, C.c_uint, _I64, _I64, _I, _I,
+                          _P, _I64] + [_P] * 9 + [_P],
+    "fp_vertex_chain_f32": [_P, _I, _P, _P, _P, _P],
     "fp_set_kernel_policy": [_I],
     "fp_launch_count": [],
     "fp_last_cuda_error": [],
     "fp_error_string": [_I],
     "fp_version": [],
 }
-_RESTYPES = {"fp_launch_count": C.c_uint64, "fp_error_string": C.c_char_p}
+_RESTYPES = {"fp_launch_count": C.c_uint64, "fp_error_string": C.c_char_p,
+             "fp_enum_pattern_count": C.c_int64}
 
 _lib = None
 

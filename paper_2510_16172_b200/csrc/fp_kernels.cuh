@@ -185,64 +185,11 @@ __device__ __forceinline__ void run_path(const PathArgs<R>& a, int64_t row, cons
   }
   uint8_t st = 0;
   P.eval(G, P.g);
-  if (OP != OP_VJP) {
-    if (P.nmin <= G.eps) st |= FP_STATUS_DEGENERATE_ENTRY;  // checked_segments (solver.py:166)
-    InvHess<R, K, MASK> H;
-    H.identity();
-    R p[NA];
-#pragma unroll
-    for (int j = 0; j < NA; ++j) p[j] = -P.g[j];  // H = I
-    for (int it = 0; it < a.iterations; ++it) {
-      bool zero;
-      const R alpha = P.step_size(G, p, a.fp_iters, zero);
-      if (zero) st |= FP_STATUS_ZERO_DIRECTION;
-      R sg[NA];
-#pragma unroll
-      for (int j = 0; j < NA; ++j) {
-        sg[j] = alpha * p[j];
-        P.t[j] = P.t[j] + sg[j];
-      }
-      R gn[NA];
-      P.eval(G, gn);
-      R y[NA];
-#pragma unroll
-      for (int j = 0; j < NA; ++j) y[j] = gn[j] - P.g[j];
-      const R sy = dot<R, K, MASK, NA>(sg, y);
-      const R ss = dot<R, K, MASK, NA>(sg, sg);
-      const R yy = dot<R, K, MASK, NA>(y, y);
-      const bool ok = sy > (R(1e-12) * sqrt_test(ss)) * sqrt_test(yy);
-      H.step(sg, y, gn, p, ok, sy);
-#pragma unroll
-      for (int j = 0; j < NA; ++j) P.g[j] = gn[j];
-      if (a.trace_len != nullptr) {
-        R q = R(0);
-#pragma unroll
-        for (int j = 0; j < NA; ++j) q = fma(P.g[j], P.g[j], q);
-        a.trace_len[(int64_t)it * a.ld + row] = P.len;
-        a.trace_gnorm[(int64_t)it * a.ld + row] = Num<R>::sqrt_(q);
-      }
-    }
-    if (a.H_out != nullptr) {
-      R* Ho = a.H_out + row * (4 * K * K);
-#pragma unroll
-      for (int i = 0; i < 2 * K; ++i)
-#pragma unroll
-        for (int j = 0; j < 2 * K; ++j) {
-          const int ii = i >> 1, ci = i & 1, jj = j >> 1, cj = j & 1;
-          const bool ai = ci == 0 || L::plane(ii), aj = cj == 0 || L::plane(jj);
-          R v = (i == j) ? R(1) : R(0);
-          if (ai && aj) v = H.h[InvHess<R, K, MASK>::id(L::idx(ii, ci), L::idx(jj, cj))];
-          Ho[i * 2 * K + j] = v;
-        }
-    }
-  }
-  // Final classification at the returned T.
-  if (!stationary<R, NA>(P.g, P.len)) st |= FP_STATUS_NOT_STATIONARY;
-  if (P.nmin <= G.eps) st |= FP_STATUS_DEGENERATE_FINAL;
-  if (P.nmin < R(1e-3)) st |= FP_STATUS_SHORT_SEGMENT;
-  bool fin = finite(P.len);
-#pragma unroll
-  for (int j = 0; j < NA; ++j) fin = fin && finite(P.t[j]) && finite(P.g[j]);
+  if (OP != OP_VJP)
+    st |= bfgs_solve<R, K, MASK>(G, P, a.iterations, a.fp_iters, a.trace_len, a.trace_gnorm, a.ld, row,
+                                 a.H_out);
+  st |= final_status<R, K, MASK>(G, P);
+  bool fin = (st & FP_STATUS_NONFINITE) == 0;
 
   R tf[K][2];
 #pragma unroll

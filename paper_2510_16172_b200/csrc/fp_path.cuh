@@ -320,6 +320,87 @@ __device__ __forceinline__ bool stationary(const R (&g)[NA], R len) {
   return Num<R>::sqrt_(q) < R(1e-5) * (R(1) + len);
 }
 
+
+// The fixed-iteration BFGS loop (solver.py:146-215) from the state P (which
+// must hold t and its evaluation). Returns DEGENERATE_ENTRY / ZERO_DIRECTION
+// status bits; optional per-iteration trace (solver.py:202-206) and final
+// inverse Hessian (return_state) in the dense 2K layout.
+template <typename R, int K, unsigned MASK>
+__device__ __forceinline__ uint8_t bfgs_solve(const Geo<R, K>& G, PathState<R, K, MASK>& P,
+                                              int iterations, int fp_iters, R* trace_len,
+                                              R* trace_gnorm, int64_t trace_ld, int64_t row,
+                                              R* H_out) {
+  using L = Lay<K, MASK>;
+  constexpr int NA = L::NA;
+  uint8_t st = 0;
+  if (P.nmin <= G.eps) st |= FP_STATUS_DEGENERATE_ENTRY;  // checked_segments (solver.py:166)
+  InvHess<R, K, MASK> H;
+  H.identity();
+  R p[NA];
+#pragma unroll
+  for (int j = 0; j < NA; ++j) p[j] = -P.g[j];  // H = I
+  for (int it = 0; it < iterations; ++it) {
+    bool zero;
+    const R alpha = P.step_size(G, p, fp_iters, zero);
+    if (zero) st |= FP_STATUS_ZERO_DIRECTION;
+    R sg[NA];
+#pragma unroll
+    for (int j = 0; j < NA; ++j) {
+      sg[j] = alpha * p[j];
+      P.t[j] = P.t[j] + sg[j];
+    }
+    R gn[NA];
+    P.eval(G, gn);
+    R y[NA];
+#pragma unroll
+    for (int j = 0; j < NA; ++j) y[j] = gn[j] - P.g[j];
+    const R sy = dot<R, K, MASK, NA>(sg, y);
+    const R ss = dot<R, K, MASK, NA>(sg, sg);
+    const R yy = dot<R, K, MASK, NA>(y, y);
+    const bool ok = sy > (R(1e-12) * sqrt_test(ss)) * sqrt_test(yy);
+    H.step(sg, y, gn, p, ok, sy);
+#pragma unroll
+    for (int j = 0; j < NA; ++j) P.g[j] = gn[j];
+    if (trace_len != nullptr) {
+      R q = R(0);
+#pragma unroll
+      for (int j = 0; j < NA; ++j) q = fma(P.g[j], P.g[j], q);
+      trace_len[int64_t(it) * trace_ld + row] = P.len;
+      trace_gnorm[int64_t(it) * trace_ld + row] = Num<R>::sqrt_(q);
+    }
+  }
+  if (H_out != nullptr) {
+    R* Ho = H_out + row * (4 * K * K);
+#pragma unroll
+    for (int i = 0; i < 2 * K; ++i)
+#pragma unroll
+      for (int j = 0; j < 2 * K; ++j) {
+        const int ii = i >> 1, ci = i & 1, jj = j >> 1, cj = j & 1;
+        const bool ai = ci == 0 || L::plane(ii), aj = cj == 0 || L::plane(jj);
+        R v = (i == j) ? R(1) : R(0);
+        if (ai && aj) v = H.h[InvHess<R, K, MASK>::id(L::idx(ii, ci), L::idx(jj, cj))];
+        Ho[i * 2 * K + j] = v;
+      }
+  }
+  return st;
+}
+
+// Classification at the returned T: stationarity gate, degenerate or short
+// segments, non-finite state.
+template <typename R, int K, unsigned MASK>
+__device__ __forceinline__ uint8_t final_status(const Geo<R, K>& G, const PathState<R, K, MASK>& P) {
+  constexpr int NA = Lay<K, MASK>::NA;
+  uint8_t st = 0;
+  if (!stationary<R, NA>(P.g, P.len)) st |= FP_STATUS_NOT_STATIONARY;
+  if (P.nmin <= G.eps) st |= FP_STATUS_DEGENERATE_FINAL;
+  if (P.nmin < R(1e-3)) st |= FP_STATUS_SHORT_SEGMENT;
+  bool fin = finite(P.len);
+#pragma unroll
+  for (int j = 0; j < NA; ++j) fin = fin && finite(P.t[j]) && finite(P.g[j]);
+  if (!fin) st |= FP_STATUS_NONFINITE;
+  return st;
+}
+
 // ---------------------------------------------------------------------------
 // Implicit-gradient VJP at the current state (objective.py:48-135,
 // implicit_diff.py:39-77). `vT` is the cotangent on T in the compressed
