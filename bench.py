@@ -409,6 +409,85 @@ def run_ours(args):
     return 0
 
 
+def run_scene(args):
+    """--workload config3 / config4: exhaustive tracing in the synthetic city.
+
+    config3: one step = enumerate + solve + bounds-mask + compact every
+    candidate of order <= 3 (value: candidate paths/s, whole job).
+    config4: one step = the config-3 trace plus the implicit VJP of sum 1/L^2
+    over valid paths, gradient scatter, vertex chain rule and the NCCL
+    all-reduce of the scene gradient (value: steps/s; ms_per_step reported).
+    """
+    import torch
+
+    from paper_2510_16172_b200 import _lib
+    from paper_2510_16172_b200.scene import DeviceScene, candidate_count, make_urban_scene, trace
+
+    ws, rank, local = _dist()
+    if ws > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    _lib.set_kernel_policy(args.policy)
+    grad = args.workload == "config4"
+    sc = make_urban_scene(seed=0, alphabet=args.alphabet)
+    ds = DeviceScene(sc)
+    total = candidate_count(sc, 3)
+    cap = 0 if args.no_records else None
+
+    def step():
+        return trace(sc, max_order=3, iterations=args.iterations, capacity=cap, with_grad=grad,
+                     device_scene=ds)
+
+    for _ in range(args.warmup):
+        res = step()
+    torch.cuda.synchronize()
+    _barrier(ws)
+    n0 = _lib.launch_count()
+    sampler = ClockSampler(torch.cuda.current_device())
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with sampler:
+        e0.record()
+        for _ in range(args.steps):
+            res = step()
+        e1.record()
+        torch.cuda.synchronize()
+    launches = _lib.launch_count() - n0
+    _barrier(ws)
+    ms = _max_over_ranks(e0.elapsed_time(e1), ws, dev) / args.steps
+    if rank == 0:
+        per_order = [{"order": o.order, "candidates": o.candidates, "converged": o.converged,
+                      "in_bounds": o.in_bounds, "valid": o.valid} for o in res.orders]
+        line = {
+            "metric": ("candidate paths/sec (exhaustive order<=3 tracing, enumerate+solve+mask+compact)"
+                       if not grad else "inverse-design gradient steps/sec (trace + implicit VJP + allreduce)"),
+            "value": (total / (ms * 1e-3)) if not grad else 1e3 / ms,
+            "unit": "paths/s" if not grad else "steps/s",
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic city (paper_2510_16172_b200.scene.make_urban_scene, seed 0)",
+            "config": {"workload": args.workload, "buildings": 16, "walls": int(sc.walls.shape[0]),
+                       "objects": sc.n_objects, "alphabet": args.alphabet, "rx": int(sc.rx.shape[0]),
+                       "candidates": total, "max_order": 3, "iterations": args.iterations,
+                       "parallelism": f"dp{ws} (contiguous candidate shares)"},
+            "orders": per_order, "valid_paths": res.valid, "gpu_launches": launches,
+            "clocks": sampler.summary(),
+        }
+        if grad:
+            line["loss"] = res.loss
+            line["grad_norm"] = float(torch.linalg.vector_norm(res.vertex_grad).item())
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0
+
+
 class _Null:
     def __enter__(self):
         return self
@@ -433,7 +512,13 @@ def main(argv=None):
     ap.add_argument("--quick", action="store_true", help="tiny CPU samples (debugging)")
     ap.add_argument("--policy", choices=("auto", "dense"), default="auto",
                     help="kernel selection (fp_set_kernel_policy)")
+    ap.add_argument("--workload", choices=("config2", "config3", "config4"), default="config2")
+    ap.add_argument("--alphabet", choices=("all", "walls"), default="all",
+                    help="config3/4 objects: walls + edges (192) or the 64 walls only")
+    ap.add_argument("--no-records", action="store_true", help="config3: counts only")
     args = ap.parse_args(argv)
+    if args.workload in ("config3", "config4") and args.impl == "ours":
+        return run_scene(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -256,7 +256,7 @@ def trace(scene: UrbanScene, max_order: int = 3, iterations: int = 20, fp_iters:
     """Enumerate, solve and mask every candidate of order 1..max_order.
 
     capacity: records kept per order (default: all candidates of that order on
-    this rank, capped at 2^24); 0 keeps counts only. with_grad: also the
+    this rank, capped at 2^26); 0 keeps counts only. with_grad: also the
     config-4 step (loss = sum 1/L^2 over valid paths and its gradient w.r.t.
     every object, TX and the wall vertices). Under torch.distributed, each
     rank takes a contiguous share of every group and (allreduce=True) the
@@ -279,44 +279,50 @@ def trace(scene: UrbanScene, max_order: int = 3, iterations: int = 20, fp_iters:
                      tx=torch.zeros(3, dtype=torch.float32, device=dev),
                      loss=torch.zeros(1, dtype=torch.float32, device=dev))
     P = lambda t: None if t is None else t.data_ptr()  # noqa: E731
-    orders = []
+    counters = torch.zeros(max_order, 4, dtype=torch.int64, device=dev)
+    recs = []
     for k in range(1, max_order + 1):
         groups = [(p, pattern_count(scene, k, p) * n_rx) for p in range(1 << k)]
         mine = sum(_share(tot, rank, world)[1] - _share(tot, rank, world)[0] for _, tot in groups)
-        cap = min(mine, 1 << 24) if capacity is None else int(capacity)
-        counters = torch.zeros(4, dtype=torch.int64, device=dev)
-        rec = dict(rx=torch.empty(cap, dtype=torch.int32, device=dev),
+        cap = min(mine, 1 << 26) if capacity is None else int(capacity)
+        rec = dict(cap=cap, rx=torch.empty(cap, dtype=torch.int32, device=dev),
                    seq=torch.empty(cap, k, dtype=torch.int32, device=dev),
                    T=torch.empty(cap, k, 2, dtype=torch.float32, device=dev),
                    L=torch.empty(cap, dtype=torch.float32, device=dev),
                    pts=torch.empty(cap, k, 3, dtype=torch.float32, device=dev) if points else None)
+        recs.append(rec)
         for p, tot in groups:
             lo, hi = _share(tot, rank, world)
             if hi <= lo:
                 continue
             rc = lib.fp_enum_trace_f32(
                 P(ds.basis), P(ds.anchor), P(ds.plane_ids), ds.n_planes, P(ds.edge_ids), ds.n_edges,
-                P(ds.tx), P(ds.rx), n_rx, k, p, lo, hi, iterations, fp_iters, P(counters), cap,
+                P(ds.tx), P(ds.rx), n_rx, k, p, lo, hi, iterations, fp_iters, P(counters[k - 1]), cap,
                 P(rec["rx"]) if cap else None, P(rec["seq"]) if cap else None,
                 P(rec["T"]) if cap else None, P(rec["L"]) if cap else None,
                 P(rec["pts"]) if cap else None,
                 P(grads["obj"]) if grads else None, P(grads["tx"]) if grads else None, None,
                 P(grads["loss"]) if grads else None, s)
             _lib.check(rc, "fp_enum_trace_f32")
-        c = reduce_sum(counters, world) if allreduce else counters
-        cand, conv, inb, valid = (int(x) for x in c.tolist())
-        n_keep = min(int(counters[3].item()), cap)
-        orders.append(OrderResult(k, cand, conv, inb, valid,
-                                  rec["rx"][:n_keep], rec["seq"][:n_keep], rec["T"][:n_keep],
-                                  rec["L"][:n_keep], rec["pts"][:n_keep] if points else None))
-    res = TraceResult(orders)
     if with_grad:
         vg = torch.zeros(scene.walls.shape[0] * 4, 3, dtype=torch.float32, device=dev)
         rc = lib.fp_vertex_chain_f32(P(grads["obj"]), N, P(ds.vert_ids), P(ds.coef), P(vg), s)
         _lib.check(rc, "fp_vertex_chain_f32")
         if allreduce:
+            # one NCCL all-reduce: wall vertices, TX, loss, object parameters (~10 KB)
             vg, grads["tx"], grads["loss"], grads["obj"] = reduce_sum_many(
                 [vg, grads["tx"], grads["loss"], grads["obj"]], world)
+    local = counters.cpu()
+    total = (reduce_sum(counters, world) if allreduce else counters).cpu()
+    orders = []
+    for k, rec in zip(range(1, max_order + 1), recs):
+        cand, conv, inb, valid = (int(x) for x in total[k - 1].tolist())
+        n_keep = min(int(local[k - 1, 3]), rec["cap"])
+        orders.append(OrderResult(k, cand, conv, inb, valid,
+                                  rec["rx"][:n_keep], rec["seq"][:n_keep], rec["T"][:n_keep],
+                                  rec["L"][:n_keep], rec["pts"][:n_keep] if points else None))
+    res = TraceResult(orders)
+    if with_grad:
         res.loss = float(grads["loss"].item())
         res.obj_grad, res.tx_grad, res.vertex_grad = grads["obj"], grads["tx"], vg
     return res
