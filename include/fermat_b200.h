@@ -166,6 +166,23 @@ int fp_enum_trace_f32(const float* obj_basis, const float* obj_anchor, const int
 int fp_vertex_chain_f32(const float* obj_grad, int n_objects, const int32_t* vert_ids,
                         const float* coef, float* vertex_grad, void* stream);
 
+/* ---- comparison solvers -------------------------------------
+ * Damped Newton on active coordinates with step halving: baselines._newton_kernel
+ * (baselines.py:152-193), the config-1 comparator. K <= 5. trace_gnorm
+ * (iterations, B) optional: |g| after each iteration. */
+int fp_newton_f32(const float* basis, const float* anchor, const float* start, const float* end,
+                  const float* T0, int64_t B, int K, int iterations, float* T_out, float* g_out,
+                  float* trace_gnorm, void* stream);
+int fp_newton_f64(const double* basis, const double* anchor, const double* start, const double* end,
+                  const double* T0, int64_t B, int K, int iterations, double* T_out, double* g_out,
+                  double* trace_gnorm, void* stream);
+/* Exact reflection points of all-plane paths: baselines.image_points_batch
+ * (baselines.py:48-71). points (B,K,3); status FP_STATUS_SINGULAR where the
+ * mirrored sight line is parallel to its plane (NoIntersection). */
+int fp_image_method_f64(const double* basis, const double* anchor, const double* start,
+                        const double* end, int64_t B, int K, double* points, uint8_t* status,
+                        void* stream);
+
 /* ---- FP32 roofline probe ----------------------------------------------------
  * blocks x 256 threads, each running iters x 128 dependent-free FFMAs; the
  * bench times it with CUDA events to measure the FP32 SIMT peak. */

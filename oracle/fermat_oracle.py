@@ -396,3 +396,93 @@ def full_gradient_rows(basis, anchor, start, end, T, rows, weights=None):
         db[j], da[j], d0[j], d1[j] = (w * x for x in sg)
         ok[j] = True
     return db, da, d0, d1, ok
+
+
+# ---------------------------------------------------------------------------
+# Comparison solvers (reference baselines.py)
+
+NEWTON_DAMPING = 1e-10      # baselines.py:127
+NEWTON_MAX_HALVINGS = 20    # baselines.py:128
+
+
+def hessian_batched(basis, anchor, start, end, T, eps):
+    """(B, 2K, 2K) Hessian with clamped norms (baselines.py:131-149)."""
+    s, nrm = clamped(basis, anchor, start, end, T, eps)
+    B, K = T.shape[0], T.shape[1]
+    u = s / nrm[..., None]
+    M = (np.eye(3, dtype=s.dtype)[None, None] - np.einsum("bki,bkj->bkij", u, u)) / nrm[..., None, None]
+    H = np.zeros((B, 2 * K, 2 * K), dtype=s.dtype)
+    for i in range(K):
+        H[:, 2 * i:2 * i + 2, 2 * i:2 * i + 2] = np.einsum(
+            "bri,brs,bsj->bij", basis[:, i], M[:, i] + M[:, i + 1], basis[:, i])
+        if i + 1 < K:
+            off = -np.einsum("bri,brs,bsj->bij", basis[:, i], M[:, i + 1], basis[:, i + 1])
+            H[:, 2 * i:2 * i + 2, 2 * i + 2:2 * i + 4] = off
+            H[:, 2 * i + 2:2 * i + 4, 2 * i:2 * i + 2] = np.swapaxes(off, 1, 2)
+    return H
+
+
+def newton(basis, anchor, start, end, T0, iterations, dtype=np.float32, trace=False):
+    """Masked damped Newton with step halving (baselines.py:152-193)."""
+    basis, anchor, start, end = (np.asarray(x).astype(dtype) for x in (basis, anchor, start, end))
+    T = np.ascontiguousarray(T0, dtype=dtype)
+    B, K = T.shape[0], T.shape[1]
+    m = 2 * K
+    eps = seg_floor(start, end, dtype)
+    active = (np.linalg.norm(basis, axis=2) > 0.0).reshape(B, m)
+    dim = active.sum(axis=1).astype(dtype)
+    g = grad_batch(basis, anchor, start, end, T, eps)
+    tg = []
+    for _ in range(iterations):
+        H = hessian_batched(basis, anchor, start, end, T, eps)
+        gm = np.where(active, g.reshape(B, m), 0.0)
+        H = np.where(active[:, :, None] & active[:, None, :], H, 0.0)
+        diag = np.arange(m)
+        tr = np.einsum("bii->b", H)
+        lam = NEWTON_DAMPING * tr / np.maximum(dim, 1.0)
+        H[:, diag, diag] = np.where(active, H[:, diag, diag] + lam[:, None], 1.0)
+        step = -np.linalg.solve(H, gm[..., None])[..., 0]
+        L0 = length_batch(basis, anchor, start, end, T)
+        scale = np.ones(B, dtype=dtype)
+        cand = T + step.reshape(B, K, 2)
+        Lc = length_batch(basis, anchor, start, end, cand)
+        for _ in range(NEWTON_MAX_HALVINGS):
+            worse = Lc > L0
+            if not np.any(worse):
+                break
+            scale = np.where(worse, scale * 0.5, scale)
+            cand = T + scale[:, None, None] * step.reshape(B, K, 2)
+            Lc = length_batch(basis, anchor, start, end, cand)
+        T = np.where((Lc <= L0)[:, None, None], cand, T)
+        g = grad_batch(basis, anchor, start, end, T, eps)
+        if trace:
+            tg.append(np.sqrt(np.einsum("bnj,bnj->b", g, g)))
+    out = dict(T=T, g=g)
+    if trace:
+        out["trace_gnorm"] = np.stack(tg)
+    return out
+
+
+def image_points(basis, anchor, start, end):
+    """Exact reflection points of all-plane paths (baselines.py:48-71), fp64."""
+    basis, anchor, start, end = (np.asarray(x, np.float64) for x in (basis, anchor, start, end))
+    B, K = basis.shape[0], basis.shape[1]
+    nrm = np.cross(basis[..., 0], basis[..., 1])
+    nrm = nrm / np.linalg.norm(nrm, axis=-1, keepdims=True)
+    imgs = np.empty((B, K, 3))
+    m = start.copy()
+    for i in range(K):
+        d = np.einsum("bi,bi->b", m - anchor[:, i], nrm[:, i])
+        m = m - 2.0 * d[:, None] * nrm[:, i]
+        imgs[:, i] = m
+    pts = np.empty((B, K, 3))
+    y = end.copy()
+    parallel = np.zeros(B, dtype=bool)
+    for i in range(K - 1, -1, -1):
+        dirv = y - imgs[:, i]
+        den = np.einsum("bi,bi->b", dirv, nrm[:, i])
+        parallel |= np.abs(den) <= 1e-12 * np.linalg.norm(dirv, axis=1)
+        t = np.einsum("bi,bi->b", anchor[:, i] - imgs[:, i], nrm[:, i]) / den
+        y = imgs[:, i] + t[:, None] * dirv
+        pts[:, i] = y
+    return pts, parallel

@@ -71,6 +71,9 @@ _SIGS = {
     "fp_enum_trace_f32": [_P, _P, _P, _I, _P, _I, _P, _P, _I, _I, C.c_uint, _I64, _I64, _I, _I,
                           _P, _I64] + [_P] * 9 + [_P],
     "fp_vertex_chain_f32": [_P, _I, _P, _P, _P, _P],
+    "fp_newton_f32": [_P] * 5 + [_I64, _I, _I] + [_P] * 3 + [_P],
+    "fp_newton_f64": [_P] * 5 + [_I64, _I, _I] + [_P] * 3 + [_P],
+    "fp_image_method_f64": [_P] * 4 + [_I64, _I, _P, _P, _P],
     "fp_set_kernel_policy": [_I],
     "fp_launch_count": [],
     "fp_last_cuda_error": [],

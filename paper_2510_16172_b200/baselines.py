@@ -1,0 +1,80 @@
+"""Comparison solvers on the GPU — drop-in for the reference's fermatpath.baselines.
+
+Mirrors /root/reference/pkg/src/fermatpath/baselines.py: the exact image
+method (baselines.py:48-80) and the masked damped Newton solver
+(baselines.py:152-201) — config 1's comparator — run as sm_100a kernels
+(csrc/fp_baselines.cu) behind fp_image_method_f64 / fp_newton_f32/f64.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .batching import BatchScene, params_tensor, ptr, stream_ptr
+from .errors import NoIntersection, NotAllPlanes
+from .geometry import PathSpec, SurfaceKind, check_params
+from .solver import Precision, SolveOptions, SolveReport
+
+
+def image_points_batch(sc: BatchScene) -> torch.Tensor:
+    """(B, K, 3) exact reflection points for all-plane scenes (baselines.py:48-71)."""
+    lib = _lib.load()
+    s64 = sc.astype(np.float64)
+    B, K = s64.size, s64.n
+    pts = torch.empty(B, K, 3, dtype=torch.float64, device=s64.basis.device)
+    st = torch.empty(B, dtype=torch.uint8, device=s64.basis.device)
+    rc = lib.fp_image_method_f64(ptr(s64.basis), ptr(s64.anchor), ptr(s64.start), ptr(s64.end), B, K,
+                                 ptr(pts), ptr(st), stream_ptr())
+    _lib.check(rc, "fp_image_method_f64")
+    if B and K and bool((st != 0).any()):
+        raise NoIntersection("mirrored sight line parallel to its plane")
+    return pts
+
+
+def image_method(spec: PathSpec) -> np.ndarray:
+    """Exact reflection points (n, 3) via successive mirroring (baselines.py:74-80)."""
+    if any(s.kind is not SurfaceKind.PLANE for s in spec.surfaces):
+        raise NotAllPlanes("image method handles planar reflections only")
+    if spec.n == 0:
+        return np.zeros((0, 3))
+    return image_points_batch(BatchScene.from_specs([spec]))[0].cpu().numpy()
+
+
+def newton_batch(sc: BatchScene, T0, opts: SolveOptions = SolveOptions(), trace: bool = False):
+    """Masked damped Newton with step halving (baselines._newton_kernel, baselines.py:152-193).
+
+    Returns (T, g[, trace_gnorm (I, B)]) as device tensors.
+    """
+    lib = _lib.load()
+    s = sc.astype(opts.precision.dtype)
+    B, K = s.size, s.n
+    dt, dev = s.basis.dtype, s.basis.device
+    T0 = torch.zeros(B, K, 2, dtype=dt, device=dev) if T0 is None else params_tensor(s, T0)
+    if K == 0:
+        out = (T0.clone(), torch.zeros_like(T0))
+        return out + ((torch.zeros(opts.iterations, B, dtype=dt, device=dev),) if trace else ())
+    T = torch.empty_like(T0)
+    g = torch.empty_like(T0)
+    tg = torch.empty(opts.iterations, B, dtype=dt, device=dev) if trace else None
+    fn = lib.fp_newton_f32 if dt == torch.float32 else lib.fp_newton_f64
+    rc = fn(ptr(s.basis), ptr(s.anchor), ptr(s.start), ptr(s.end), ptr(T0), B, K, opts.iterations,
+            ptr(T), ptr(g), ptr(tg), stream_ptr())
+    _lib.check(rc, "fp_newton")
+    return (T, g, tg) if trace else (T, g)
+
+
+def newton_solve(spec: PathSpec, T0, opts: SolveOptions = SolveOptions()) -> SolveReport:
+    """Damped Newton on active coordinates with step halving (baselines.py:196-201)."""
+    T0 = check_params(spec, T0)
+    sc = BatchScene.from_specs([spec])
+    T, g = newton_batch(sc, T0[None], opts)
+    from .batching import objective_batch
+
+    L = float(objective_batch(sc.astype(opts.precision.dtype), T)[0].item())
+    if opts.precision is Precision.SINGLE:
+        L = float(np.float32(L))
+    return SolveReport(solution=T[0].double().cpu().numpy(), final_length=L,
+                       final_grad_norm=float(np.linalg.norm(g[0].cpu().numpy())),
+                       iterations=opts.iterations)

@@ -1,0 +1,71 @@
+"""GPU comparison solvers (damped Newton, image method) vs the reference's golden outputs."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2510_16172_b200 as fp
+from paper_2510_16172_b200.baselines import image_method, image_points_batch, newton_batch, newton_solve
+from paper_2510_16172_b200.batching import BatchScene
+from paper_2510_16172_b200.solver import Precision, SolveOptions
+from oracle import fermat_oracle as O
+
+from parity import converged_mask, golden, points_ok
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("K", [1, 2, 3])
+def test_newton_fp32_config1(K):
+    d = golden(f"config1_k{K}")
+    sc = BatchScene(d["basis"], d["anchor"], d["start"], d["end"])
+    f = np.float64
+    for it in (5, 10, 20):
+        T, g, tg = newton_batch(sc, d["T0"], SolveOptions(iterations=it, precision=Precision.SINGLE),
+                                trace=True)
+        Tref = d[f"newton_T_{it}"]
+        conv = converged_mask(d["basis"], d["anchor"], d["start"], d["end"], Tref)
+        pts = O.path_points(*(x.astype(f) for x in (d["basis"], d["anchor"], d["start"], d["end"])),
+                            T.double().cpu().numpy())[:, 1:-1]
+        ref = O.path_points(*(x.astype(f) for x in (d["basis"], d["anchor"], d["start"], d["end"])),
+                            Tref.astype(f))[:, 1:-1]
+        ok = points_ok(pts, ref)
+        assert ok[conv].all()
+        assert ok.mean() >= 0.9
+        # residual-gradient curve: the final trace entry is the returned |g|
+        gn = np.linalg.norm(g.cpu().numpy().reshape(len(T), -1), axis=1)
+        assert np.array_equal(tg[-1].cpu().numpy(), gn.astype(np.float32))
+
+
+@pytest.mark.parametrize("kinds", ["reflections", "diffractions", "mixed"])
+def test_newton_fp64_reference_scenes(kinds):
+    for n in (1, 3, 5):
+        d = golden(f"refgen_{kinds}_n{n}")
+        sc = BatchScene(d["basis"], d["anchor"], d["start"], d["end"])
+        T, _ = newton_batch(sc, d["T0"], SolveOptions(iterations=10, precision=Precision.DOUBLE))
+        assert np.allclose(T.cpu().numpy(), d["newton_T_f64"], rtol=1e-9, atol=1e-9)
+
+
+def test_image_method():
+    for n in (1, 3, 5):
+        d = golden(f"refgen_reflections_n{n}")
+        pts = image_points_batch(BatchScene(d["basis"], d["anchor"], d["start"], d["end"]))
+        assert np.allclose(pts.cpu().numpy(), d["image_points"], rtol=1e-12, atol=1e-12)
+    # known answers (test_baselines.py:32-39,64-82)
+    spec = fp.PathSpec(start=[-1.0, 1.0, 0.0], end=[1.0, 1.0, 0.0],
+                       surfaces=(fp.make_plane([0.0, 0.0, 0.0], [1, 0, 0], [0, 0, 1]),))
+    assert np.allclose(image_method(spec), [[0.0, 0.0, 0.0]], atol=1e-14)
+    with pytest.raises(fp.NotAllPlanes):
+        image_method(fp.PathSpec(start=[0, 0, 1], end=[1, 0, 1],
+                                 surfaces=(fp.make_edge([0.5, 0, 0], [0, 1, 0]),)))
+    with pytest.raises(fp.NoIntersection):
+        image_method(fp.PathSpec(start=[0.0, 0.0, 1.0], end=[1.0, 0.0, -1.0],
+                                 surfaces=(fp.make_plane([0.0, 0.0, 0.0], [1, 0, 0], [0, 1, 0]),)))
+
+
+def test_newton_scalar_converges():
+    d = golden("refgen_mixed_n3")
+    from test_gpu_solve import _specs
+    for spec, T0 in list(zip(_specs(d), d["T0"]))[:4]:
+        rep = newton_solve(spec, T0, SolveOptions(iterations=30))
+        assert rep.final_grad_norm < 1e-10 * (1 + rep.final_length)

@@ -120,3 +120,39 @@ def test_degenerate_entry_raises():
     with pytest.raises(O.OracleDegenerate):
         O.bfgs(basis, np.zeros((1, 1, 3)), np.zeros((1, 3)), np.array([[0.0, 0.0, 2.0]]),
                np.zeros((1, 1, 2)), 3, 1, np.float64)
+
+
+@pytest.mark.parametrize("K", [1, 2, 3])
+def test_newton_config1(K):
+    d = golden(f"config1_k{K}")
+    for it in (5, 10, 20):
+        r = O.newton(d["basis"], d["anchor"], d["start"], d["end"], d["T0"], it, np.float32)
+        assert _eq(r["T"], d[f"newton_T_{it}"], _same_numpy(d))
+        assert _eq(r["g"], d[f"newton_g_{it}"], _same_numpy(d))
+
+
+@pytest.mark.parametrize("kinds", ["reflections", "diffractions", "mixed"])
+def test_newton_and_image_reference_scenes(kinds):
+    for n in (1, 3, 5):
+        d = golden(f"refgen_{kinds}_n{n}")
+        r = O.newton(d["basis"], d["anchor"], d["start"], d["end"], d["T0"], 10, np.float64)
+        assert _eq(r["T"], d["newton_T_f64"], _same_numpy(d))
+        if kinds == "reflections":
+            pts, par = O.image_points(d["basis"], d["anchor"], d["start"], d["end"])
+            assert not par.any()
+            assert _eq(pts, d["image_points"], _same_numpy(d))
+
+
+def test_enumeration_oracle_self_consistent():
+    from oracle import enumerate_oracle as E
+    kinds = np.array([True, True, False, True, False])
+    planes, edges = np.nonzero(kinds)[0], np.nonzero(~kinds)[0]
+    for order in (1, 2, 3):
+        got = set()
+        for p in E.patterns(order):
+            seqs = E.pattern_sequences(planes, edges, order, p)
+            assert len({tuple(s) for s in seqs}) == len(seqs)
+            assert all(kinds[s[j]] == bool((p >> j) & 1) for s in seqs for j in range(order))
+            got |= {tuple(s) for s in seqs}
+        assert got == E.brute_force_sequences(kinds, order)
+        assert len(got) == len(kinds) * (len(kinds) - 1) ** (order - 1)
