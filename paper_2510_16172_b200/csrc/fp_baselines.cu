@@ -31,6 +31,40 @@ __device__ __forceinline__ R length_at(const Geo<R, K>& G, const R (&t)[K][2]) {
   return L;
 }
 
+// Reference-exact gradient with clamped norms (batching.py:95-104): IEEE
+// sqrt and division (no fast reciprocal), so the comparator's residual
+// gradients carry the reference's rounding, not the hot path's.
+template <typename R, int K>
+__device__ __forceinline__ void grad_exact(const Geo<R, K>& G, const R (&t)[2 * K], R (&s)[K + 1][3],
+                                           R (&nc)[K + 1], R (&g)[2 * K]) {
+  R P[K + 2][3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    P[0][r] = G.x0[r];
+    P[K + 1][r] = G.xe[r];
+  }
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int r = 0; r < 3; ++r) P[i + 1][r] = fma(G.A[i][r][1], t[2 * i + 1], G.A[i][r][0] * t[2 * i]) + G.b[i][r];
+  R u[K + 1][3];
+#pragma unroll
+  for (int k = 0; k <= K; ++k) {
+#pragma unroll
+    for (int r = 0; r < 3; ++r) s[k][r] = P[k + 1][r] - P[k][r];
+    nc[k] = clamp_floor(Num<R>::sqrt_(fma(s[k][2], s[k][2], fma(s[k][1], s[k][1], s[k][0] * s[k][0]))), G.eps);
+#pragma unroll
+    for (int r = 0; r < 3; ++r) u[k][r] = Num<R>::div(s[k][r], nc[k]);
+  }
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const R q0 = u[i][0] - u[i + 1][0], q1 = u[i][1] - u[i + 1][1], q2 = u[i][2] - u[i + 1][2];
+      g[2 * i + c] = fma(G.A[i][2][c], q2, fma(G.A[i][1][c], q1, G.A[i][0][c] * q0));
+    }
+}
+
 // Damped Newton on active coordinates with step halving (baselines.py:152-193):
 // H from clamped segments (hessian_batch, baselines.py:131-149), inert rows
 // and columns pinned to the identity, damping 1e-10 tr(H_a) / dim(active),
@@ -41,11 +75,14 @@ __global__ void __launch_bounds__(kThreads) newton_kernel(const R* basis, const 
                                                           int64_t B, int iterations, R* T_out,
                                                           R* g_out, R* trace_gnorm) {
   constexpr unsigned MASK = (1u << K) - 1u;  // dense layout: t[i][c] = P.t[2i + c]
+  (void)MASK;
   const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (b >= B) return;
   Geo<R, K> G;
   load_geo<R, K, MASK>(G, basis + b * 6 * K, anchor + b * 3 * K, start + 3 * b, end + 3 * b);
-  PathState<R, K, MASK> P;
+  struct {
+    R t[2 * K], g[2 * K], s[K + 1][3], nc[K + 1];
+  } P;
 #pragma unroll
   for (int j = 0; j < 2 * K; ++j) P.t[j] = T0[b * 2 * K + j];
   bool act[K][2];
@@ -57,40 +94,60 @@ __global__ void __launch_bounds__(kThreads) newton_kernel(const R* basis, const 
       act[i][c] = G.A[i][0][c] != R(0) || G.A[i][1][c] != R(0) || G.A[i][2][c] != R(0);
       dim += act[i][c];
     }
-  P.eval(G, P.g);
+  grad_exact<R, K>(G, P.t, P.s, P.nc, P.g);
   for (int it = 0; it < iterations; ++it) {
-    // Hessian blocks at the current T (clamped norms, as hessian_batch).
-    R u[K + 1][3];
+    // Hessian blocks at the current T as hessian_batch computes them
+    // (baselines.py:131-149): M_k = (I - u_k u_k^T) / n_k with clamped norms,
+    // diagonal A_i^T (M_i + M_{i+1}) A_i, off-diagonal -A_i^T M_{i+1} A_{i+1}.
+    R M[K + 1][6];  // symmetric 3x3: xx, xy, xz, yy, yz, zz
 #pragma unroll
-    for (int k = 0; k <= K; ++k)
+    for (int k = 0; k <= K; ++k) {
+      R u[3];
 #pragma unroll
-      for (int r = 0; r < 3; ++r) u[k][r] = P.s[k][r] * P.rn[k];
+      for (int r = 0; r < 3; ++r) u[r] = Num<R>::div(P.s[k][r], P.nc[k]);
+      const int ri[6] = {0, 0, 0, 1, 1, 2}, ci[6] = {0, 1, 2, 1, 2, 2};
+#pragma unroll
+      for (int e = 0; e < 6; ++e)
+        M[k][e] = Num<R>::div((ri[e] == ci[e] ? R(1) : R(0)) - u[ri[e]] * u[ci[e]], P.nc[k]);
+    }
+    auto mget = [&](const R* m, int r, int c) -> R {
+      const int lo = r < c ? r : c, hi = r < c ? c : r;
+      return m[lo == 0 ? hi : (lo == 1 ? 2 + hi : 5)];
+    };
     R D[K][3], O[K][2][2];
     R tr = R(0);
 #pragma unroll
     for (int i = 0; i < K; ++i) {
-      R ai[2], ao[2], gii[3];
+      R Ms[6];
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        ai[c] = fma(G.A[i][2][c], u[i][2], fma(G.A[i][1][c], u[i][1], G.A[i][0][c] * u[i][0]));
-        ao[c] = fma(G.A[i][2][c], u[i + 1][2], fma(G.A[i][1][c], u[i + 1][1], G.A[i][0][c] * u[i + 1][0]));
-      }
-      gii[0] = fma(G.A[i][2][0], G.A[i][2][0], fma(G.A[i][1][0], G.A[i][1][0], G.A[i][0][0] * G.A[i][0][0]));
-      gii[1] = fma(G.A[i][2][0], G.A[i][2][1], fma(G.A[i][1][0], G.A[i][1][1], G.A[i][0][0] * G.A[i][0][1]));
-      gii[2] = fma(G.A[i][2][1], G.A[i][2][1], fma(G.A[i][1][1], G.A[i][1][1], G.A[i][0][1] * G.A[i][0][1]));
-      D[i][0] = (gii[0] - ai[0] * ai[0]) * P.rn[i] + (gii[0] - ao[0] * ao[0]) * P.rn[i + 1];
-      D[i][1] = (gii[1] - ai[0] * ai[1]) * P.rn[i] + (gii[1] - ao[0] * ao[1]) * P.rn[i + 1];
-      D[i][2] = (gii[2] - ai[1] * ai[1]) * P.rn[i] + (gii[2] - ao[1] * ao[1]) * P.rn[i + 1];
+      for (int e = 0; e < 6; ++e) Ms[e] = M[i][e] + M[i + 1][e];
+      R Dm[2][2];
+#pragma unroll
+      for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int y = 0; y < 2; ++y) {
+          R acc = R(0);
+#pragma unroll
+          for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) acc = fma(G.A[i][r][x] * mget(Ms, r, c), G.A[i][c][y], acc);
+          Dm[x][y] = acc;
+        }
+      D[i][0] = Dm[0][0];
+      D[i][1] = Dm[0][1];
+      D[i][2] = Dm[1][1];
       if (i + 1 < K) {
 #pragma unroll
         for (int x = 0; x < 2; ++x)
 #pragma unroll
           for (int y = 0; y < 2; ++y) {
-            R an = fma(G.A[i + 1][2][y], u[i + 1][2],
-                       fma(G.A[i + 1][1][y], u[i + 1][1], G.A[i + 1][0][y] * u[i + 1][0]));
-            const R gij = fma(G.A[i][2][x], G.A[i + 1][2][y],
-                              fma(G.A[i][1][x], G.A[i + 1][1][y], G.A[i][0][x] * G.A[i + 1][0][y]));
-            O[i][x][y] = (act[i][x] && act[i + 1][y]) ? -(gij - ao[x] * an) * P.rn[i + 1] : R(0);
+            R acc = R(0);
+#pragma unroll
+            for (int r = 0; r < 3; ++r)
+#pragma unroll
+              for (int c = 0; c < 3; ++c)
+                acc = fma(G.A[i][r][x] * mget(M[i + 1], r, c), G.A[i + 1][c][y], acc);
+            O[i][x][y] = (act[i][x] && act[i + 1][y]) ? -acc : R(0);
           }
       }
       if (act[i][0]) tr += D[i][0];
@@ -173,7 +230,7 @@ __global__ void __launch_bounds__(kThreads) newton_kernel(const R* basis, const 
         P.t[2 * i + 1] = cand[i][1];
       }
     }
-    P.eval(G, P.g);
+    grad_exact<R, K>(G, P.t, P.s, P.nc, P.g);
     if (trace_gnorm) {
       R q = R(0);
 #pragma unroll
