@@ -488,6 +488,68 @@ def run_scene(args):
     return 0
 
 
+def run_config1(args):
+    """--workload config1: diffraction-only K=1,2,3, 2^20 paths each; residual
+    gradient norm vs iteration for the BFGS solver and the damped-Newton
+    comparator (GPU; plus the reference's Newton restated on the CPU for a
+    4096-path sample), iterations 5/10/20. value: BFGS paths/s at K=3, I=20."""
+    import torch
+
+    from paper_2510_16172_b200 import _lib, datagen
+    from paper_2510_16172_b200.baselines import newton_batch
+    from paper_2510_16172_b200.batching import BatchScene
+    from paper_2510_16172_b200.solver import Precision, SolveOptions, solve
+    from oracle import fermat_oracle as O
+
+    torch.cuda.set_device(0)
+    _lib.set_kernel_policy(args.policy)
+    rows, value = [], None
+    for K in (1, 2, 3):
+        b = datagen.config1(K, args.paths if args.paths != 1 << 22 else 1 << 20)
+        sc = BatchScene(b.basis, b.anchor, b.start, b.end)
+        T0 = torch.zeros(b.size, K, 2, device="cuda")
+        sub = slice(0, 4096)
+        for I in (5, 10, 20):
+            opts = SolveOptions(iterations=I, precision=Precision.SINGLE)
+            tr = solve(sc, T0, SolveOptions(iterations=I, precision=Precision.SINGLE, record_trace=True))
+            med_bfgs = torch.median(tr.trace_gnorm, dim=1).values.tolist()
+            conv_b = float(tr.converged.float().mean().item())
+            _, gN, tgN = newton_batch(sc, T0, opts, trace=True)
+            med_newt = torch.median(tgN, dim=1).values.tolist()
+            for _ in range(args.warmup):
+                solve(sc, T0, opts, want_grad=False, want_points=False)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(args.steps):
+                solve(sc, T0, opts, want_grad=False, want_points=False)
+            e1.record()
+            torch.cuda.synchronize()
+            bfgs_s = e0.elapsed_time(e1) * 1e-3 / args.steps
+            e0.record()
+            for _ in range(max(1, args.steps // 3)):
+                newton_batch(sc, T0, opts)
+            e1.record()
+            torch.cuda.synchronize()
+            newt_s = e0.elapsed_time(e1) * 1e-3 / max(1, args.steps // 3)
+            ref = O.newton(b.basis[sub], b.anchor[sub], b.start[sub], b.end[sub], b.T0[sub], I,
+                           np.float32, trace=True)
+            med_ref = np.median(ref["trace_gnorm"], axis=1).tolist()
+            rows.append({"K": K, "iterations": I, "paths": b.size,
+                         "bfgs_median_grad_norm": med_bfgs, "newton_median_grad_norm": med_newt,
+                         "reference_newton_cpu_median_grad_norm_4096": med_ref,
+                         "bfgs_converged_fraction": conv_b,
+                         "bfgs_paths_per_s": b.size / bfgs_s, "newton_paths_per_s": b.size / newt_s})
+            if K == 3 and I == 20:
+                value = b.size / bfgs_s
+    line = {"metric": "paths/sec (diffraction-only BFGS, K=3, 20 it) + residual-gradient curves",
+            "value": value, "unit": "paths/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (SURVEY §8(d) generator, D-only)",
+            "config": {"workload": "config1: D-only K=1,2,3, 2^20 paths, I=5/10/20"}, "rows": rows}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 class _Null:
     def __enter__(self):
         return self
@@ -512,13 +574,16 @@ def main(argv=None):
     ap.add_argument("--quick", action="store_true", help="tiny CPU samples (debugging)")
     ap.add_argument("--policy", choices=("auto", "dense"), default="auto",
                     help="kernel selection (fp_set_kernel_policy)")
-    ap.add_argument("--workload", choices=("config2", "config3", "config4"), default="config2")
+    ap.add_argument("--workload", choices=("config1", "config2", "config3", "config4"),
+                    default="config2")
     ap.add_argument("--alphabet", choices=("all", "walls"), default="all",
                     help="config3/4 objects: walls + edges (192) or the 64 walls only")
     ap.add_argument("--no-records", action="store_true", help="config3: counts only")
     args = ap.parse_args(argv)
     if args.workload in ("config3", "config4") and args.impl == "ours":
         return run_scene(args)
+    if args.workload == "config1" and args.impl == "ours":
+        return run_config1(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)
