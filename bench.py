@@ -561,7 +561,7 @@ class _Null:
 def main(argv=None):
     ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--order", type=int, default=3)
@@ -572,7 +572,7 @@ def main(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="tiny CPU samples (debugging)")
-    ap.add_argument("--policy", choices=("auto", "dense"), default="auto",
+    ap.add_argument("--policy", choices=("auto", "dense", "serial"), default="auto",
                     help="kernel selection (fp_set_kernel_policy)")
     ap.add_argument("--workload", choices=("config1", "config2", "config3", "config4"),
                     default="config2")

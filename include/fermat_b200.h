@@ -195,6 +195,9 @@ int fp_peak_ffma(int blocks, int iters, float* out, void* stream);
  * kernel (identical results, used by the tests to prove it). */
 #define FP_POLICY_AUTO 0
 #define FP_POLICY_DENSE 1
+/* as AUTO, but the per-mask kernels run one after another on the caller's
+ * stream instead of on concurrent side streams */
+#define FP_POLICY_AUTO_SERIAL 2
 int fp_set_kernel_policy(int policy);
 
 /* Number of kernels this library has launched in the process (monotone). */

@@ -101,7 +101,7 @@ template <typename R>
 static int dispatch(int K, const PathArgs<R>& a, int op, cudaStream_t s, bool allow_bucketing = true) {
   constexpr bool is_f32 = sizeof(R) == sizeof(float);
   const int64_t B = a.B;
-  const bool bucketed = is_f32 && allow_bucketing && g_policy.load() == FP_POLICY_AUTO && K >= 1 &&
+  const bool bucketed = is_f32 && allow_bucketing && g_policy.load() != FP_POLICY_DENSE && K >= 1 &&
                         K <= kMaxSpecialisedOrder && (op == OP_SOLVE || op == OP_SOLVE_VJP) &&
                         B > 0 && B < (int64_t(1) << 31) && a.rows == nullptr;
   if (!bucketed) return dispatch_dense_k<R>(K, a, op, s);
@@ -113,7 +113,7 @@ static int dispatch(int K, const PathArgs<R>& a, int op, cudaStream_t s, bool al
     int live = 0;
     for (int m = 0; m < plan.nb; ++m) live += plan.count[m] > 0;
     SideStreams& ss = side_streams();
-    const bool fan = live > 1;
+    const bool fan = live > 1 && g_policy.load() != FP_POLICY_AUTO_SERIAL;
     if (e == cudaSuccess && fan) e = ss.fork(s, live);
     int k = 0;
     for (unsigned m = 0; m < unsigned(plan.nb) && e == cudaSuccess; ++m) {
@@ -588,7 +588,8 @@ int fp_init_params_f64(const double* basis, const double* anchor, const double* 
 uint64_t fp_launch_count(void) { return g_launches.load(); }
 
 int fp_set_kernel_policy(int policy) {
-  if (policy != FP_POLICY_AUTO && policy != FP_POLICY_DENSE) return FP_ERR_INVALID_ARGUMENT;
+  if (policy != FP_POLICY_AUTO && policy != FP_POLICY_DENSE && policy != FP_POLICY_AUTO_SERIAL)
+    return FP_ERR_INVALID_ARGUMENT;
   g_policy.store(policy);
   return FP_OK;
 }

@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(kThreads, (MinBlocks<float, Lay<K, MASK>::NA>:
         inb = inb && fabsf(P.t[L::idx(i, 0)]) <= 1.f;
         if (L::plane(i)) inb = inb && fabsf(P.t[L::idx(i, 1)]) <= 1.f;
       }
-      len = P.len;
+      len = P.length();
     }
     const bool valid = live && conv && inb;
     // ---- counters and compaction (warp-aggregated) -------------------------

@@ -133,6 +133,19 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// TMA bulk store shared -> global (bulk_group completion) for the output slabs.
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit_and_wait_read() {
+  asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 __device__ __forceinline__ bool aligned16(const void* p) {
   return (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
 }
@@ -219,7 +232,7 @@ __device__ __forceinline__ void run_path(const PathArgs<R>& a, int64_t row, cons
 #pragma unroll
         for (int r = 0; r < 3; ++r) o.pts[3 * i + r] = X[i + 1][r];
     }
-    if (o.len) o.len[0] = P.len;
+    if (o.len) o.len[0] = P.length();
   }
   if (OP != OP_SOLVE) {
     R vf[K][2];
@@ -354,6 +367,7 @@ __device__ __forceinline__ void process_tile(const PathArgs<R>& a, const int32_t
     const int64_t row = srow ? int64_t(srow[tid]) : base + tid;
     run_path<R, K, MASK, OP>(a, row, in, has_v, tid, true);
   }
+  fence_async_smem();  // make the slab writes visible to the TMA (async) proxy
   __syncthreads();
 
   R* oT = reinterpret_cast<R*>(smem);
@@ -366,6 +380,35 @@ __device__ __forceinline__ void process_tile(const PathArgs<R>& a, const int32_t
   R* od1 = od0 + kThreads * 3;
   R* ou = od1 + kThreads * 3;
   uint8_t* ost = reinterpret_cast<uint8_t*>(smem + size_t(Wk::slab_elems) * kThreads * sizeof(R));
+  // Full contiguous tiles with 16-byte aligned destinations leave with one TMA
+  // bulk store per slab; others with cooperative (scattering) stores.
+  if (srow == nullptr && n == kThreads &&
+      (!a.T_out || aligned16(a.T_out + base * Wk::T)) && (!a.g_out || aligned16(a.g_out + base * Wk::T)) &&
+      (!a.points_out || aligned16(a.points_out + base * Wk::pts)) &&
+      (!a.length_out || aligned16(a.length_out + base)) &&
+      (!a.d_basis || aligned16(a.d_basis + base * Wk::basis)) &&
+      (!a.d_anchor || aligned16(a.d_anchor + base * Wk::anchor)) &&
+      (!a.d_start || aligned16(a.d_start + base * 3)) && (!a.d_end || aligned16(a.d_end + base * 3)) &&
+      (!a.u_out || aligned16(a.u_out + base * Wk::T)) &&
+      (!a.status_out || aligned16(a.status_out + base))) {
+    if (tid == 0) {
+      constexpr uint32_t bT = kThreads * Wk::T * sizeof(R), bP = kThreads * Wk::pts * sizeof(R),
+                         bL = kThreads * sizeof(R), bB = kThreads * Wk::basis * sizeof(R),
+                         bA = kThreads * Wk::anchor * sizeof(R), bV = kThreads * 3 * sizeof(R);
+      if (a.T_out) bulk_s2g(a.T_out + base * Wk::T, oT, bT);
+      if (a.g_out) bulk_s2g(a.g_out + base * Wk::T, og, bT);
+      if (a.points_out) bulk_s2g(a.points_out + base * Wk::pts, op, bP);
+      if (a.length_out) bulk_s2g(a.length_out + base, ol, bL);
+      if (a.d_basis) bulk_s2g(a.d_basis + base * Wk::basis, odb, bB);
+      if (a.d_anchor) bulk_s2g(a.d_anchor + base * Wk::anchor, oda, bA);
+      if (a.d_start) bulk_s2g(a.d_start + base * 3, od0, bV);
+      if (a.d_end) bulk_s2g(a.d_end + base * 3, od1, bV);
+      if (a.u_out) bulk_s2g(a.u_out + base * Wk::T, ou, bT);
+      if (a.status_out) bulk_s2g(a.status_out + base, ost, kThreads);
+      bulk_commit_and_wait_read();
+    }
+    return;
+  }
   if (a.T_out) tile_out<R, Wk::T>(a.T_out, oT, srow, base, n);
   if (a.g_out) tile_out<R, Wk::T>(a.g_out, og, srow, base, n);
   if (a.points_out) tile_out<R, Wk::pts>(a.points_out, op, srow, base, n);

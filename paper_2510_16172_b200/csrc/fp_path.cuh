@@ -67,9 +67,22 @@ struct PathState {
   R g[NA];     // clamped-norm gradient at t
   R s[S][3];   // segments at t
   R rn[S];     // 1 / max(|s_k|, eps)
-  R nc[S];     // max(|s_k|, eps)
-  R len;       // sum of unclamped norms (path length)
-  R nmin;      // smallest unclamped norm
+  R nu[S];     // |s_k| (unclamped)
+
+  // Path length: sum of unclamped norms (batching.py:123-126).
+  __device__ __forceinline__ R length() const {
+    R l = nu[0];
+#pragma unroll
+    for (int k = 1; k < S; ++k) l += nu[k];
+    return l;
+  }
+  // Shortest segment (NaN-blind like the reference's `norms <= eps` test).
+  __device__ __forceinline__ R min_norm() const {
+    R m = nu[0];
+#pragma unroll
+    for (int k = 1; k < S; ++k) m = nu[k] < m ? nu[k] : m;
+    return m;
+  }
 
   // x_i = A_i t_i + b_i (geometry.py:153-165)
   __device__ __forceinline__ void points(const Geo<R, K>& G, R (&P)[K + 2][3]) const {
@@ -93,8 +106,6 @@ struct PathState {
   __device__ __forceinline__ void eval(const Geo<R, K>& G, R (&gout)[NA]) {
     R P[K + 2][3];
     points(G, P);
-    len = R(0);
-    nmin = Num<R>::inf();
     R u[S][3];
 #pragma unroll
     for (int k = 0; k < S; ++k) {
@@ -103,10 +114,8 @@ struct PathState {
       R q = s[k][0] * s[k][0];
       q = fma(s[k][1], s[k][1], q);
       q = fma(s[k][2], s[k][2], q);
-      R n;
-      norm_rcp(q, G.eps, G.reps, n, nc[k], rn[k]);
-      len += n;
-      nmin = n < nmin ? n : nmin;
+      R nc;
+      norm_rcp(q, G.eps, G.reps, nu[k], nc, rn[k]);
 #pragma unroll
       for (int r = 0; r < 3; ++r) u[k][r] = s[k][r] * rn[k];
     }
@@ -149,23 +158,23 @@ struct PathState {
       for (int r = 0; r < 3; ++r) d[k][r] = w[k][r] - w[k - 1][r];
     }
     R a2[S], c[S];
-    R total = R(0);
+    R total;
 #pragma unroll
     for (int k = 0; k < S; ++k) {
       a2[k] = fma(d[k][2], d[k][2], fma(d[k][1], d[k][1], d[k][0] * d[k][0]));
       c[k] = fma(d[k][2], s[k][2], fma(d[k][1], s[k][1], d[k][0] * s[k][0]));
-      total += a2[k];
+      total = k == 0 ? a2[0] : total + a2[k];
     }
     zero = total <= Num<R>::tiny();
     R alpha = R(0);
     {
-      R num = R(0), den = R(0);
+      R num = c[0] * rn[0], den = a2[0] * rn[0];
 #pragma unroll
-      for (int k = 0; k < S; ++k) {
+      for (int k = 1; k < S; ++k) {
         num = fma(c[k], rn[k], num);
         den = fma(a2[k], rn[k], den);
       }
-      const R cand = -Num<R>::div(num, zero ? R(1) : den);
+      const R cand = -div_fast(num, zero ? R(1) : den);
       alpha = (zero || !finite(cand)) ? alpha : cand;
     }
     for (int f = 1; f < fp_iters; ++f) {
@@ -177,10 +186,10 @@ struct PathState {
         const R e2 = fma(alpha, d[k][2], s[k][2]);
         R n0, n, ri;
         norm_rcp(fma(e2, e2, fma(e1, e1, e0 * e0)), G.eps, G.reps, n0, n, ri);
-        num = fma(c[k], ri, num);
-        den = fma(a2[k], ri, den);
+        num = k == 0 ? c[0] * ri : fma(c[k], ri, num);
+        den = k == 0 ? a2[0] * ri : fma(a2[k], ri, den);
       }
-      const R cand = -Num<R>::div(num, zero ? R(1) : den);
+      const R cand = -div_fast(num, zero ? R(1) : den);
       alpha = (zero || !finite(cand)) ? alpha : cand;
     }
     return alpha;
@@ -266,7 +275,7 @@ struct InvHess {
       R Hy[NA];
 #pragma unroll
       for (int i = 0; i < NA; ++i) Hy[i] = Hg[i] + p[i];
-      const R rho = Num<R>::rcp(sy);
+      const R rho = rcp_fast(sy);
       const R yHy = dot<R, K, MASK, NA>(y, Hy);
       const R half = R(0.5) * fma(rho * rho, yHy, rho);
       R z[NA];
@@ -333,7 +342,7 @@ __device__ __forceinline__ uint8_t bfgs_solve(const Geo<R, K>& G, PathState<R, K
   using L = Lay<K, MASK>;
   constexpr int NA = L::NA;
   uint8_t st = 0;
-  if (P.nmin <= G.eps) st |= FP_STATUS_DEGENERATE_ENTRY;  // checked_segments (solver.py:166)
+  if (P.min_norm() <= G.eps) st |= FP_STATUS_DEGENERATE_ENTRY;  // checked_segments (solver.py:166)
   InvHess<R, K, MASK> H;
   H.identity();
   R p[NA];
@@ -365,7 +374,7 @@ __device__ __forceinline__ uint8_t bfgs_solve(const Geo<R, K>& G, PathState<R, K
       R q = R(0);
 #pragma unroll
       for (int j = 0; j < NA; ++j) q = fma(P.g[j], P.g[j], q);
-      trace_len[int64_t(it) * trace_ld + row] = P.len;
+      trace_len[int64_t(it) * trace_ld + row] = P.length();
       trace_gnorm[int64_t(it) * trace_ld + row] = Num<R>::sqrt_(q);
     }
   }
@@ -391,10 +400,11 @@ template <typename R, int K, unsigned MASK>
 __device__ __forceinline__ uint8_t final_status(const Geo<R, K>& G, const PathState<R, K, MASK>& P) {
   constexpr int NA = Lay<K, MASK>::NA;
   uint8_t st = 0;
-  if (!stationary<R, NA>(P.g, P.len)) st |= FP_STATUS_NOT_STATIONARY;
-  if (P.nmin <= G.eps) st |= FP_STATUS_DEGENERATE_FINAL;
-  if (P.nmin < R(1e-3)) st |= FP_STATUS_SHORT_SEGMENT;
-  bool fin = finite(P.len);
+  const R len = P.length(), nmin = P.min_norm();
+  if (!stationary<R, NA>(P.g, len)) st |= FP_STATUS_NOT_STATIONARY;
+  if (nmin <= G.eps) st |= FP_STATUS_DEGENERATE_FINAL;
+  if (nmin < R(1e-3)) st |= FP_STATUS_SHORT_SEGMENT;
+  bool fin = finite(len);
 #pragma unroll
   for (int j = 0; j < NA; ++j) fin = fin && finite(P.t[j]) && finite(P.g[j]);
   if (!fin) st |= FP_STATUS_NONFINITE;
@@ -529,7 +539,7 @@ __device__ __forceinline__ uint8_t implicit_vjp(const Geo<R, K>& G, const PathSt
         }
         const R det = C0 * C2 - C1 * C1;
         ok = ok && (det > R(0)) && finite(det);
-        const R id = Num<R>::rcp(det);
+        const R id = rcp_fast(det);
         Ci[i][0] = C2 * id;
         Ci[i][1] = -C1 * id;
         Ci[i][2] = C0 * id;
