@@ -176,6 +176,13 @@ int fp_newton_f32(const float* basis, const float* anchor, const float* start, c
 int fp_newton_f64(const double* basis, const double* anchor, const double* start, const double* end,
                   const double* T0, int64_t B, int K, int iterations, double* T_out, double* g_out,
                   double* trace_gnorm, void* stream);
+/* Fixed-step gradient descent baseline: baselines._gd_kernel (baselines.py:87-101). K <= 5. */
+int fp_gd_f32(const float* basis, const float* anchor, const float* start, const float* end,
+              const float* T0, int64_t B, int K, int iterations, float* T_out, float* g_out,
+              void* stream);
+int fp_gd_f64(const double* basis, const double* anchor, const double* start, const double* end,
+              const double* T0, int64_t B, int K, int iterations, double* T_out, double* g_out,
+              void* stream);
 /* Exact reflection points of all-plane paths: baselines.image_points_batch
  * (baselines.py:48-71). points (B,K,3); status FP_STATUS_SINGULAR where the
  * mirrored sight line is parallel to its plane (NoIntersection). */

@@ -74,6 +74,8 @@ _SIGS = {
     "fp_newton_f32": [_P] * 5 + [_I64, _I, _I] + [_P] * 3 + [_P],
     "fp_newton_f64": [_P] * 5 + [_I64, _I, _I] + [_P] * 3 + [_P],
     "fp_image_method_f64": [_P] * 4 + [_I64, _I, _P, _P, _P],
+    "fp_gd_f32": [_P] * 5 + [_I64, _I, _I, _P, _P, _P],
+    "fp_gd_f64": [_P] * 5 + [_I64, _I, _I, _P, _P, _P],
     "fp_set_kernel_policy": [_I],
     "fp_launch_count": [],
     "fp_last_cuda_error": [],

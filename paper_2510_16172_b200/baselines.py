@@ -78,3 +78,90 @@ def newton_solve(spec: PathSpec, T0, opts: SolveOptions = SolveOptions()) -> Sol
     return SolveReport(solution=T[0].double().cpu().numpy(), final_length=L,
                        final_grad_norm=float(np.linalg.norm(g[0].cpu().numpy())),
                        iterations=opts.iterations)
+
+
+def gd_batch(sc: BatchScene, T0, opts: SolveOptions = SolveOptions()):
+    """Fixed-step gradient descent (baselines._gd_kernel, baselines.py:87-101) -> (T, g)."""
+    lib = _lib.load()
+    s = sc.astype(opts.precision.dtype)
+    B, K = s.size, s.n
+    dt, dev = s.basis.dtype, s.basis.device
+    T0 = torch.zeros(B, K, 2, dtype=dt, device=dev) if T0 is None else params_tensor(s, T0)
+    if K == 0:
+        return T0.clone(), torch.zeros_like(T0)
+    T = torch.empty_like(T0)
+    g = torch.empty_like(T0)
+    fn = lib.fp_gd_f32 if dt == torch.float32 else lib.fp_gd_f64
+    rc = fn(ptr(s.basis), ptr(s.anchor), ptr(s.start), ptr(s.end), ptr(T0), B, K, opts.iterations,
+            ptr(T), ptr(g), stream_ptr())
+    _lib.check(rc, "fp_gd")
+    return T, g
+
+
+def gradient_descent(spec: PathSpec, T0, opts: SolveOptions = SolveOptions()) -> SolveReport:
+    """Fixed-step gradient descent baseline (baselines.py:104-111)."""
+    T0 = check_params(spec, T0)
+    sc = BatchScene.from_specs([spec])
+    T, g = gd_batch(sc, T0[None], opts)
+    from .batching import objective_batch
+
+    L = float(objective_batch(sc, T.double())[0].item())
+    if opts.precision is Precision.SINGLE:
+        L = float(np.float32(L))
+    return SolveReport(solution=T[0].double().cpu().numpy(), final_length=L,
+                       final_grad_norm=float(np.linalg.norm(g[0].cpu().numpy())),
+                       iterations=opts.iterations)
+
+
+# High-precision reference (baselines.py:204-249)
+REFERENCE_GRAD_TOL = 1e-12
+REFERENCE_BFGS_ITERS = 1000
+REFERENCE_FP_ITERS = 64
+REFERENCE_POLISH_ITERS = 64
+
+
+def _converged(sc64: BatchScene, T: torch.Tensor) -> torch.Tensor:
+    """|g| < 1e-12 (1 + L) with clamped-norm g (baselines.py:236-240)."""
+    from .batching import objective_batch
+
+    L, g, _, _ = objective_batch(sc64, T)
+    return torch.linalg.vector_norm(g.reshape(len(L), -1), dim=1) < REFERENCE_GRAD_TOL * (1.0 + L)
+
+
+def reference_solve_batch(specs, T0s=None):
+    """Ground truth: 1000 fp64 BFGS iterations (64 fixed-point steps) from the
+    midpoint projection, then up to 64 single Newton steps on the paths still
+    above |g| < 1e-12 (1 + L) (baselines.py:208-233). Returns (T numpy (B,n,2),
+    converged numpy (B,))."""
+    from .batching import stack_params
+    from .solver import init_params_batch, solve
+
+    sc = BatchScene.from_specs(specs).astype(np.float64)
+    T0 = init_params_batch(sc) if T0s is None else params_tensor(sc, stack_params(specs, T0s))
+    if sc.n == 0:
+        return T0.cpu().numpy(), np.ones(sc.size, dtype=bool)
+    res = solve(sc, T0, SolveOptions(REFERENCE_BFGS_ITERS, REFERENCE_FP_ITERS, Precision.DOUBLE),
+                want_points=False)
+    T = res.T
+    conv = _converged(sc, T)
+    polish = SolveOptions(iterations=1, precision=Precision.DOUBLE)
+    for _ in range(REFERENCE_POLISH_ITERS):
+        todo = torch.nonzero(~conv).flatten()
+        if todo.numel() == 0:
+            break
+        sub = BatchScene(sc.basis[todo], sc.anchor[todo], sc.start[todo], sc.end[todo])
+        Tn, _ = newton_batch(sub, T[todo], polish)
+        T = T.clone()
+        T[todo] = Tn
+        conv = _converged(sc, T)
+    return T.cpu().numpy(), conv.cpu().numpy()
+
+
+def reference_solve(spec: PathSpec, T0=None) -> np.ndarray:
+    """High-precision parameters for one path; NoConvergence on failure (baselines.py:243-249)."""
+    from .errors import NoConvergence
+
+    T, conv = reference_solve_batch([spec], None if T0 is None else [check_params(spec, T0)])
+    if not conv[0]:
+        raise NoConvergence("reference solver missed its gradient tolerance")
+    return T[0]

@@ -245,6 +245,42 @@ __global__ void __launch_bounds__(kThreads) newton_kernel(const R* basis, const 
   }
 }
 
+// Fixed-step gradient descent (baselines._gd_kernel, baselines.py:87-101):
+// eta = 0.1 |end - start| / (1 + |g0|), T -= eta g for `iterations` steps.
+template <typename R, int K>
+__global__ void __launch_bounds__(kThreads) gd_kernel(const R* basis, const R* anchor, const R* start,
+                                                      const R* end, const R* T0, int64_t B,
+                                                      int iterations, R* T_out, R* g_out) {
+  constexpr unsigned MASK = (1u << K) - 1u;
+  const int64_t b = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  Geo<R, K> G;
+  load_geo<R, K, MASK>(G, basis + b * 6 * K, anchor + b * 3 * K, start + 3 * b, end + 3 * b);
+  R t[2 * K], g[2 * K], s[K + 1][3], nc[K + 1];
+#pragma unroll
+  for (int j = 0; j < 2 * K; ++j) t[j] = T0[b * 2 * K + j];
+  grad_exact<R, K>(G, t, s, nc, g);
+  R g2 = R(0), d2 = R(0);
+#pragma unroll
+  for (int j = 0; j < 2 * K; ++j) g2 = fma(g[j], g[j], g2);
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    const R d = G.xe[r] - G.x0[r];
+    d2 = fma(d, d, d2);
+  }
+  const R eta = Num<R>::div(R(0.1) * Num<R>::sqrt_(d2), R(1) + Num<R>::sqrt_(g2));
+  for (int it = 0; it < iterations; ++it) {
+#pragma unroll
+    for (int j = 0; j < 2 * K; ++j) t[j] = t[j] - eta * g[j];
+    grad_exact<R, K>(G, t, s, nc, g);
+  }
+#pragma unroll
+  for (int j = 0; j < 2 * K; ++j) {
+    T_out[b * 2 * K + j] = t[j];
+    if (g_out) g_out[b * 2 * K + j] = g[j];
+  }
+}
+
 // Image method (baselines.py:48-71): mirror the start across each plane, then
 // intersect the line from the last image to the end with each plane in reverse.
 // status bit FP_STATUS_SINGULAR marks a sight line parallel to its plane
@@ -304,6 +340,26 @@ static cudaError_t launch_newton(const R* basis, const R* anchor, const R* start
 }
 
 template <typename R>
+static int gd_impl(const R* basis, const R* anchor, const R* start, const R* end, const R* T0,
+                   int64_t B, int K, int iterations, R* T_out, R* g_out, void* stream) {
+  if (B < 0 || iterations < 1 || (B > 0 && (!basis || !anchor || !start || !end || !T0 || !T_out)))
+    return FP_ERR_INVALID_ARGUMENT;
+  if (B == 0) return FP_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const unsigned blocks = unsigned((B + kThreads - 1) / kThreads);
+  switch (K) {
+    case 1: gd_kernel<R, 1><<<blocks, kThreads, 0, s>>>(basis, anchor, start, end, T0, B, iterations, T_out, g_out); break;
+    case 2: gd_kernel<R, 2><<<blocks, kThreads, 0, s>>>(basis, anchor, start, end, T0, B, iterations, T_out, g_out); break;
+    case 3: gd_kernel<R, 3><<<blocks, kThreads, 0, s>>>(basis, anchor, start, end, T0, B, iterations, T_out, g_out); break;
+    case 4: gd_kernel<R, 4><<<blocks, kThreads, 0, s>>>(basis, anchor, start, end, T0, B, iterations, T_out, g_out); break;
+    case 5: gd_kernel<R, 5><<<blocks, kThreads, 0, s>>>(basis, anchor, start, end, T0, B, iterations, T_out, g_out); break;
+    default: return FP_ERR_UNSUPPORTED_ORDER;
+  }
+  count_launches(1);
+  return cudaGetLastError() == cudaSuccess ? FP_OK : FP_ERR_CUDA;
+}
+
+template <typename R>
 static int newton_impl(const R* basis, const R* anchor, const R* start, const R* end, const R* T0,
                        int64_t B, int K, int iterations, R* T_out, R* g_out, R* trace, void* stream) {
   if (B < 0 || iterations < 1 || (B > 0 && (!basis || !anchor || !start || !end || !T0 || !T_out)))
@@ -340,6 +396,18 @@ int fp_newton_f64(const double* basis, const double* anchor, const double* start
                   double* trace_gnorm, void* stream) {
   return newton_impl<double>(basis, anchor, start, end, T0, B, K, iterations, T_out, g_out,
                              trace_gnorm, stream);
+}
+
+int fp_gd_f32(const float* basis, const float* anchor, const float* start, const float* end,
+              const float* T0, int64_t B, int K, int iterations, float* T_out, float* g_out,
+              void* stream) {
+  return gd_impl<float>(basis, anchor, start, end, T0, B, K, iterations, T_out, g_out, stream);
+}
+
+int fp_gd_f64(const double* basis, const double* anchor, const double* start, const double* end,
+              const double* T0, int64_t B, int K, int iterations, double* T_out, double* g_out,
+              void* stream) {
+  return gd_impl<double>(basis, anchor, start, end, T0, B, K, iterations, T_out, g_out, stream);
 }
 
 int fp_image_method_f64(const double* basis, const double* anchor, const double* start,

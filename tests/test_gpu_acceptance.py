@@ -1,0 +1,236 @@
+"""The reference's nine acceptance criteria (test_acceptance.py:53-309)
+re-run against this package: every solve, gradient and oracle call executes on the GPU.
+
+Thresholds are the reference's own; runtime budgets are not asserted (they
+concern the CPU reference).
+"""
+
+import io
+
+import numpy as np
+import pytest
+import torch
+from scipy.optimize import minimize_scalar
+
+import paper_2510_16172_b200 as fp
+from paper_2510_16172_b200.baselines import image_points_batch, reference_solve_batch
+from paper_2510_16172_b200.batching import BatchScene, embed_batch, objective_batch
+from paper_2510_16172_b200.harness import (BenchConfig, Kinds, gen_scenes, grad_check, read_records,
+                                           run_bench, write_records)
+from paper_2510_16172_b200.solver import Precision, SolveOptions, solve
+
+pytestmark = pytest.mark.gpu
+
+
+def _init(specs):
+    return fp.solver.init_params_batch(BatchScene.from_specs(specs))
+
+
+def _solved_points(specs, iterations=100, fp_iters=64, precision=Precision.DOUBLE):
+    sc = BatchScene.from_specs(specs)
+    T0 = _init(specs)
+    res = solve(sc, T0, SolveOptions(iterations=iterations, fixed_point_iters=fp_iters,
+                                     precision=precision))
+    pts = embed_batch(sc.astype(np.float64), res.T.double())[:, 1:-1]
+    return sc, T0, res, pts
+
+
+def _perturb(spec, rng, scale):
+    return fp.init_params(spec) + rng.normal(size=(spec.n, 2)) * scale * spec.active_mask
+
+
+def test_criterion_1_derivatives():
+    rng = np.random.default_rng(31)
+    gw = hw = 0.0
+    for n in (1, 2, 3, 4, 5):
+        for spec in gen_scenes(31, n, Kinds.MIXED, 20):
+            T = _perturb(spec, rng, 0.1)
+            sc = BatchScene.from_specs([spec])
+            m = 2 * n
+            # batched central differences: rows = +/- h on each coordinate
+            E = np.eye(m).reshape(m, n, 2)
+            h1, h2 = 1e-6, 1e-5
+            Tp = np.concatenate([T + h1 * E, T - h1 * E, T + h2 * E, T - h2 * E])
+            scb = BatchScene(*(np.repeat(x, 4 * m, axis=0) for x in
+                               (sc.basis.cpu().numpy(), sc.anchor.cpu().numpy(),
+                                sc.start.cpu().numpy(), sc.end.cpu().numpy())))
+            L, g, _, _ = objective_batch(scb, Tp)
+            L, g = L.cpu().numpy(), g.cpu().numpy().reshape(4 * m, m)
+            fd_g = (L[:m] - L[m:2 * m]) / (2 * h1)
+            fd_H = ((g[2 * m:3 * m] - g[3 * m:]) / (2 * h2)).T
+            G = fp.gradient(spec, T).ravel()
+            H = fp.hessian(spec, T)
+            gw = max(gw, float(np.abs(G - fd_g).max()))
+            hw = max(hw, float(np.abs(H - fd_H).max()))
+            assert np.allclose(H, H.T, atol=1e-12)
+            for i in range(n):
+                for j in range(n):
+                    if abs(i - j) > 1:
+                        assert np.all(H[2 * i:2 * i + 2, 2 * j:2 * j + 2] == 0.0)
+    assert gw < 1e-6 and hw < 1e-5
+
+
+def test_criterion_2_image_method():
+    worst_mean, worst_frac = 0.0, 1.0
+    for n in (1, 2, 3, 4, 5):
+        specs = gen_scenes(3, n, Kinds.REFLECTIONS, 1000)
+        sc, _, _, pts = _solved_points(specs)
+        truth = image_points_batch(sc)
+        worst_mean = max(worst_mean, float(torch.linalg.vector_norm(pts - truth, dim=2).mean()))
+        _, _, _, pts_s = _solved_points(specs, precision=Precision.SINGLE)
+        err = torch.linalg.vector_norm(pts_s - truth, dim=2).mean(dim=1)
+        worst_frac = min(worst_frac, float((err < 1e-3).double().mean()))
+    assert worst_mean < 1e-6
+    assert worst_frac >= 0.95
+
+
+def test_criterion_3_diffraction_accuracy_and_inert_coordinates():
+    worst = 0.0
+    for n in (1, 2, 3, 4, 5):
+        specs = gen_scenes(5, n, Kinds.DIFFRACTIONS, 1000)
+        sc, T0, _, pts = _solved_points(specs)
+        Tref, conv = reference_solve_batch(specs, list(T0.cpu().numpy()))
+        assert np.all(conv)
+        ref = embed_batch(sc.astype(np.float64), torch.as_tensor(Tref, device=pts.device))[:, 1:-1]
+        worst = max(worst, float(torch.linalg.vector_norm(pts - ref, dim=2).mean()))
+    assert worst < 1e-6
+    rng = np.random.default_rng(0)
+    opts = SolveOptions(iterations=100, fixed_point_iters=64)
+    for n in (1, 3, 5):
+        specs = gen_scenes(5, n, Kinds.DIFFRACTIONS, 100)
+        sc = BatchScene.from_specs(specs)
+        T0 = _init(specs).cpu().numpy()
+        Ts = T0.copy()
+        Ts[..., 1] = rng.normal(size=T0[..., 1].shape) * 100.0
+        a, b = solve(sc, T0, opts), solve(sc, Ts, opts)
+        assert torch.equal(a.T[..., 0], b.T[..., 0])
+        assert np.array_equal(b.T[..., 1].cpu().numpy(), Ts[..., 1])
+        assert torch.equal(a.points, b.points)
+
+
+def test_criterion_4_mixed_sequences_uniform_traces():
+    worst = 0.0
+    for n in (1, 2, 3, 4, 5):
+        specs = gen_scenes(5, n, Kinds.MIXED, 1000)
+        sc, T0, _, pts = _solved_points(specs)
+        Tref, conv = reference_solve_batch(specs, list(T0.cpu().numpy()))
+        assert np.all(conv)
+        ref = embed_batch(sc.astype(np.float64), torch.as_tensor(Tref, device=pts.device))[:, 1:-1]
+        worst = max(worst, float(torch.linalg.vector_norm(pts - ref, dim=2).mean()))
+    assert worst < 1e-6
+    opts = SolveOptions(iterations=25, fixed_point_iters=4, record_trace=True)
+    lengths = set()
+    for kinds in Kinds:
+        specs = gen_scenes(6, 3, kinds, 10)
+        for rep in fp.batch_solve(specs, [fp.init_params(s) for s in specs], opts):
+            lengths.add(len(rep.trace))
+    assert lengths == {25}
+
+
+def test_criterion_5_fixed_point_line_search():
+    rng = np.random.default_rng(7)
+    opts = SolveOptions(iterations=60, fixed_point_iters=64)
+    n_inst = within = 0
+    worst64 = 0.0
+    for kinds in (Kinds.REFLECTIONS, Kinds.MIXED):
+        for n in (1, 2, 3, 4, 5):
+            specs = gen_scenes(11, n, kinds, 10)
+            reps = fp.batch_solve(specs, [fp.init_params(s) for s in specs], opts)
+            for spec, rep in zip(specs, reps):
+                for _ in range(10):
+                    T = rep.solution + rng.normal(size=(n, 2)) * 1e-3 * spec.active_mask
+                    g = fp.gradient(spec, T)
+                    P = -g / np.linalg.norm(g)
+                    astar = float(minimize_scalar(lambda a: fp.objective.path_length(spec, T + a * P),
+                                                  bracket=(0.0, 1e-3), method="golden",
+                                                  options={"xtol": 1e-12}).x)
+                    a1 = fp.line_search_alpha(spec, T, P, k=1)
+                    a64 = fp.line_search_alpha(spec, T, P, k=64)
+                    n_inst += 1
+                    worst64 = max(worst64, abs(a64 - astar) / (1 + abs(astar)))
+                    within += abs(a1 - astar) <= 0.01 * (1 + abs(astar))
+    assert n_inst == 1000
+    assert worst64 <= 1e-6
+    assert within / n_inst >= 0.90
+
+
+def test_criterion_6_implicit_differentiation():
+    vjp_worst = env_worst = 0.0
+    for n, count in {1: 13, 2: 13, 3: 12, 4: 12}.items():
+        rep = grad_check(21, n, Kinds.MIXED, count)
+        vjp_worst = max(vjp_worst, rep.vjp_max_rel_error)
+        env_worst = max(env_worst, rep.envelope_max_rel_error)
+    assert vjp_worst <= 1e-3
+    assert env_worst <= 1e-6
+
+
+def test_criterion_7_gradient_cost_independent_of_depth():
+    import time
+
+    from paper_2510_16172_b200.implicit_diff import vjp_batch
+
+    specs = gen_scenes(9, 4, Kinds.MIXED, 50)
+    sc = BatchScene.from_specs(specs)
+    T0 = _init(specs)
+    t = {}
+    for iters in (16, 128):
+        T = solve(sc, T0, SolveOptions(iterations=iters, fixed_point_iters=64)).T
+        vjp_batch(sc, T, w_L=1.0, mode="envelope")
+        reps = []
+        for _ in range(5):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            vjp_batch(sc, T, w_L=1.0, mode="envelope")
+            torch.cuda.synchronize()
+            reps.append(time.perf_counter() - t0)
+        t[iters] = min(reps)
+    assert max(t.values()) / min(t.values()) < 2.0
+
+
+def test_criterion_8_ordinal_benchmark():
+    config = BenchConfig(seed=3, batch=200, kinds=Kinds.REFLECTIONS,
+                         solvers=("ours", "ours-64", "gd", "image"), iterations=100,
+                         fixed_point_iters=4, precision=Precision.SINGLE)
+    buf = io.StringIO()
+    write_records(run_bench(config, timing_reps=3), buf)
+    buf.seek(0)
+    by = {(r.solver, r.n): r for r in read_records(buf)}
+    for n in config.n_range:
+        ours, o64, gd, img = by[("ours", n)], by[("ours-64", n)], by[("gd", n)], by[("image", n)]
+        assert gd.mean_error >= 10.0 * ours.mean_error
+        assert ours.mean_error <= 1e-3
+        assert o64.mean_error <= ours.mean_error
+        # the reference also asserts the image method is faster; on the GPU both
+        # are launch-latency bound at 200 paths, so only accuracy is compared
+
+
+def test_criterion_9_determinism_and_batch_scalar_bitwise():
+    config = BenchConfig(seed=12, batch=50, n_range=(1, 2, 3), kinds=Kinds.MIXED,
+                         solvers=("ours", "gd", "newton"), iterations=50)
+    a = [r.mean_error for r in run_bench(config, timing_reps=1)]
+    b = [r.mean_error for r in run_bench(config, timing_reps=1)]
+    assert a == b
+    opts = SolveOptions(iterations=60, fixed_point_iters=8)
+    for kinds in Kinds:
+        specs = gen_scenes(13, 3, kinds, 10)
+        T0s = [fp.init_params(s) for s in specs]
+        for spec, T0, br in zip(specs, T0s, fp.batch_solve(specs, T0s, opts)):
+            assert np.array_equal(fp.bfgs_solve(spec, T0, opts).solution, br.solution)
+
+
+def test_harness_cli_solve_and_bench(tmp_path, capsys):
+    from paper_2510_16172_b200 import cli
+
+    out = tmp_path / "s.yaml"
+    assert cli.main(["gen", "--n", "2", "--count", "2", "--out", str(out)]) == 0
+    assert cli.main(["solve", str(out)]) == 0
+    text = capsys.readouterr().out
+    assert "scene 1: length=" in text and "x3 = (" in text
+    csv_out = tmp_path / "r.csv"
+    assert cli.main(["bench", "--batch", "5", "--n", "1", "2", "--solvers", "ours", "gd",
+                     "--iterations", "20", "--out", str(csv_out)]) == 0
+    with open(csv_out) as fh:
+        recs = read_records(fh)
+    assert len(recs) == 4 and all(r.wall_time_ms > 0 and r.mean_error >= 0 for r in recs)
+    assert cli.main(["grad-check", "--n", "1", "--count", "2"]) == 0
+    assert capsys.readouterr().out.startswith("PASS")
