@@ -141,6 +141,7 @@ template <typename R>
 static PathArgs<R> blank_args() {
   PathArgs<R> a;
   std::memset(&a, 0, sizeof(a));
+  a.nz = R(-0.0);
   return a;
 }
 

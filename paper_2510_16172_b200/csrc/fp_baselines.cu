@@ -11,7 +11,7 @@ namespace fp {
 // Unclamped total length at parameters t (batching.py:123-126).
 template <typename R, int K>
 __device__ __forceinline__ R length_at(const Geo<R, K>& G, const R (&t)[K][2]) {
-  R prev[3] = {G.x0[0], G.x0[1], G.x0[2]};
+  R prev[3] = {G.x0(0), G.x0(1), G.x0(2)};
   R L = R(0);
 #pragma unroll
   for (int i = 0; i <= K; ++i) {
@@ -19,9 +19,9 @@ __device__ __forceinline__ R length_at(const Geo<R, K>& G, const R (&t)[K][2]) {
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
       if (i < K)
-        x[r] = fma(G.A[i][r][1], t[i][1], G.A[i][r][0] * t[i][0]) + G.b[i][r];
+        x[r] = fma(G.A(i, r, 1), t[i][1], G.A(i, r, 0) * t[i][0]) + G.b(i, r);
       else
-        x[r] = G.xe[r];
+        x[r] = G.xe(r);
     }
     const R d0 = x[0] - prev[0], d1 = x[1] - prev[1], d2 = x[2] - prev[2];
     L += Num<R>::sqrt_(fma(d2, d2, fma(d1, d1, d0 * d0)));
@@ -40,13 +40,13 @@ __device__ __forceinline__ void grad_exact(const Geo<R, K>& G, const R (&t)[2 * 
   R P[K + 2][3];
 #pragma unroll
   for (int r = 0; r < 3; ++r) {
-    P[0][r] = G.x0[r];
-    P[K + 1][r] = G.xe[r];
+    P[0][r] = G.x0(r);
+    P[K + 1][r] = G.xe(r);
   }
 #pragma unroll
   for (int i = 0; i < K; ++i)
 #pragma unroll
-    for (int r = 0; r < 3; ++r) P[i + 1][r] = fma(G.A[i][r][1], t[2 * i + 1], G.A[i][r][0] * t[2 * i]) + G.b[i][r];
+    for (int r = 0; r < 3; ++r) P[i + 1][r] = fma(G.A(i, r, 1), t[2 * i + 1], G.A(i, r, 0) * t[2 * i]) + G.b(i, r);
   R u[K + 1][3];
 #pragma unroll
   for (int k = 0; k <= K; ++k) {
@@ -61,7 +61,7 @@ __device__ __forceinline__ void grad_exact(const Geo<R, K>& G, const R (&t)[2 * 
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
       const R q0 = u[i][0] - u[i + 1][0], q1 = u[i][1] - u[i + 1][1], q2 = u[i][2] - u[i + 1][2];
-      g[2 * i + c] = fma(G.A[i][2][c], q2, fma(G.A[i][1][c], q1, G.A[i][0][c] * q0));
+      g[2 * i + c] = fma(G.A(i, 2, c), q2, fma(G.A(i, 1, c), q1, G.A(i, 0, c) * q0));
     }
 }
 
@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(kThreads) newton_kernel(const R* basis, const 
   for (int i = 0; i < K; ++i)
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
-      act[i][c] = G.A[i][0][c] != R(0) || G.A[i][1][c] != R(0) || G.A[i][2][c] != R(0);
+      act[i][c] = G.A(i, 0, c) != R(0) || G.A(i, 1, c) != R(0) || G.A(i, 2, c) != R(0);
       dim += act[i][c];
     }
   grad_exact<R, K>(G, P.t, P.s, P.nc, P.g);
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kThreads) newton_kernel(const R* basis, const 
 #pragma unroll
           for (int r = 0; r < 3; ++r)
 #pragma unroll
-            for (int c = 0; c < 3; ++c) acc = fma(G.A[i][r][x] * mget(Ms, r, c), G.A[i][c][y], acc);
+            for (int c = 0; c < 3; ++c) acc = fma(G.A(i, r, x) * mget(Ms, r, c), G.A(i, c, y), acc);
           Dm[x][y] = acc;
         }
       D[i][0] = Dm[0][0];
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(kThreads) newton_kernel(const R* basis, const 
             for (int r = 0; r < 3; ++r)
 #pragma unroll
               for (int c = 0; c < 3; ++c)
-                acc = fma(G.A[i][r][x] * mget(M[i + 1], r, c), G.A[i + 1][c][y], acc);
+                acc = fma(G.A(i, r, x) * mget(M[i + 1], r, c), G.A(i + 1, c, y), acc);
             O[i][x][y] = (act[i][x] && act[i + 1][y]) ? -acc : R(0);
           }
       }
@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(kThreads) gd_kernel(const R* basis, const R* a
   for (int j = 0; j < 2 * K; ++j) g2 = fma(g[j], g[j], g2);
 #pragma unroll
   for (int r = 0; r < 3; ++r) {
-    const R d = G.xe[r] - G.x0[r];
+    const R d = G.xe(r) - G.x0(r);
     d2 = fma(d, d, d2);
   }
   const R eta = Num<R>::div(R(0.1) * Num<R>::sqrt_(d2), R(1) + Num<R>::sqrt_(g2));

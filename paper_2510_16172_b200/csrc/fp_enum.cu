@@ -32,6 +32,7 @@ namespace fp {
 
 struct EnumArgs {
   const float *obj_basis, *obj_anchor;  // (N,3,2), (N,3)
+  float nz;                             // -0 (Geo::nz)
   const int32_t *plane_ids, *edge_ids;
   int n_planes, n_edges;
   const float *tx, *rx;  // (3), (n_rx,3)
@@ -96,8 +97,8 @@ __global__ void __launch_bounds__(kThreads, (MinBlocks<float, Lay<K, MASK>::NA>:
         x1[e] = __ldg(a.rx + 3 * rx + e);
       }
       load_geo<float, K, MASK>(G, bb, aa, x0, x1);
-#pragma unroll
-      for (int j = 0; j < NA; ++j) P.t[j] = 0.f;
+      G.nz = a.nz;
+      P.zero_t();
       P.eval(G, P.g);
       uint8_t st = bfgs_solve<float, K, MASK>(G, P, a.iterations, a.fp_iters, nullptr, nullptr, 0, 0,
                                               nullptr);
@@ -106,8 +107,8 @@ __global__ void __launch_bounds__(kThreads, (MinBlocks<float, Lay<K, MASK>::NA>:
       inb = true;
 #pragma unroll
       for (int i = 0; i < K; ++i) {
-        inb = inb && fabsf(P.t[L::idx(i, 0)]) <= 1.f;
-        if (L::plane(i)) inb = inb && fabsf(P.t[L::idx(i, 1)]) <= 1.f;
+        inb = inb && fabsf(P.T(L::idx(i, 0))) <= 1.f;
+        if (L::plane(i)) inb = inb && fabsf(P.T(L::idx(i, 1))) <= 1.f;
       }
       len = P.length();
     }
@@ -131,8 +132,8 @@ __global__ void __launch_bounds__(kThreads, (MinBlocks<float, Lay<K, MASK>::NA>:
         for (int i = 0; i < K; ++i) {
           if (a.rec_seq) a.rec_seq[pos * K + i] = obj[i];
           if (a.rec_T) {
-            a.rec_T[pos * 2 * K + 2 * i] = P.t[L::idx(i, 0)];
-            a.rec_T[pos * 2 * K + 2 * i + 1] = L::plane(i) ? P.t[L::idx(i, 1)] : 0.f;
+            a.rec_T[pos * 2 * K + 2 * i] = P.T(L::idx(i, 0));
+            a.rec_T[pos * 2 * K + 2 * i + 1] = L::plane(i) ? P.T(L::idx(i, 1)) : 0.f;
           }
         }
         if (a.rec_L) a.rec_L[pos] = len;
@@ -156,8 +157,8 @@ __global__ void __launch_bounds__(kThreads, (MinBlocks<float, Lay<K, MASK>::NA>:
         float tf[K][2], vf[K][2];
 #pragma unroll
         for (int i = 0; i < K; ++i) {
-          tf[i][0] = P.t[L::idx(i, 0)];
-          tf[i][1] = L::plane(i) ? P.t[L::idx(i, 1)] : 0.f;
+          tf[i][0] = P.T(L::idx(i, 0));
+          tf[i][1] = L::plane(i) ? P.T(L::idx(i, 1)) : 0.f;
           vf[i][0] = vf[i][1] = 0.f;
         }
         SceneGrad<float, K> sg;
@@ -282,6 +283,7 @@ static int fill_args(EnumArgs& a, const float* obj_basis, const float* obj_ancho
       cand_end < cand_begin)
     return FP_ERR_INVALID_ARGUMENT;
   std::memset(&a, 0, sizeof(a));
+  a.nz = -0.0f;
   a.obj_basis = obj_basis;
   a.obj_anchor = obj_anchor;
   a.plane_ids = plane_ids;

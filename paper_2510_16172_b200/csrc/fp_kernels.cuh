@@ -23,6 +23,7 @@ struct PathArgs {
   const R* vT;      // VJP-only: cotangent on T (B,K,2), may be null
   const R* wL;      // per-path weight on L, may be null
   R wL_scale;       // weight used when wL is null
+  R nz;             // -0 (Geo::nz: keeps ptxas from contracting paired products)
   int mode;         // fp_vjp_mode
   int64_t B;        // staged mode: rows [row_begin, B) of the batch
   int64_t row_begin;
@@ -188,12 +189,14 @@ __device__ __forceinline__ void run_path(const PathArgs<R>& a, int64_t row, cons
   constexpr int NA = L::NA;
   Geo<R, K> G;
   load_geo<R, K, MASK>(G, in.b, in.a, in.x0, in.x1);
+  G.nz = a.nz;
   PathState<R, K, MASK> P;
   R tin[K];
+  P.zero_t();
 #pragma unroll
   for (int i = 0; i < K; ++i) {
-    P.t[L::idx(i, 0)] = in.T[2 * i];
-    if (L::plane(i)) P.t[L::idx(i, 1)] = in.T[2 * i + 1];
+    P.T(L::idx(i, 0)) = in.T[2 * i];
+    if (L::plane(i)) P.T(L::idx(i, 1)) = in.T[2 * i + 1];
     tin[i] = in.T[2 * i + 1];
   }
   uint8_t st = 0;
@@ -207,8 +210,8 @@ __device__ __forceinline__ void run_path(const PathArgs<R>& a, int64_t row, cons
   R tf[K][2];
 #pragma unroll
   for (int i = 0; i < K; ++i) {
-    tf[i][0] = P.t[L::idx(i, 0)];
-    tf[i][1] = L::plane(i) ? P.t[L::idx(i, 1)] : tin[i];
+    tf[i][0] = P.T(L::idx(i, 0));
+    tf[i][1] = L::plane(i) ? P.T(L::idx(i, 1)) : tin[i];
   }
   const Outs<R> o = make_outs<R, K>(a, row, tid, staged);
   if (OP != OP_VJP) {
@@ -221,8 +224,8 @@ __device__ __forceinline__ void run_path(const PathArgs<R>& a, int64_t row, cons
     if (o.g)
 #pragma unroll
       for (int i = 0; i < K; ++i) {
-        o.g[2 * i] = P.g[L::idx(i, 0)];
-        o.g[2 * i + 1] = L::plane(i) ? P.g[L::idx(i, 1)] : R(0);
+        o.g[2 * i] = P.Gr(L::idx(i, 0));
+        o.g[2 * i + 1] = L::plane(i) ? P.Gr(L::idx(i, 1)) : R(0);
       }
     if (o.pts) {
       R X[K + 2][3];

@@ -5,8 +5,20 @@
 // plane with two unknowns; clear: an edge with one). MASK = all ones is the
 // "dense" uniform 2K formulation of the reference (geometry.py:86-90): edges
 // carry a zero second basis column, which produces exact zeros, so it is
-// valid for every batch; specialised masks skip the inert lanes and give the
-// same bits for those paths.
+// valid for every batch; specialised masks skip the inert lanes.
+//
+// Paired arithmetic: the loop is issue-bound (ncu: warps eligible but not
+// selected, FMA pipe ~50%), so the state is laid out for the sm_100 paired
+// FP32 instructions FFMA2 / FMUL2 / FADD2 (two IEEE operations per issue,
+// a scalar operand broadcast and negations for free):
+//   * 3-vectors as an (x, y) pair plus a scalar z; the basis A_i as column
+//     pairs {A_0c, A_1c} plus A_2c, so A t, A p and points are paired;
+//   * vectors over the NA unknowns as NA/2 pairs (odd NA: the last hi lane
+//     is padding and never read);
+//   * the inverse Hessian as row pairs {h(2m, c), h(2m+1, c)} of its upper
+//     triangle (c >= 2m), so the rank-two update and H v are paired.
+// Each lane rounds exactly like the scalar operation it replaces. fp64 runs
+// the same code with the pair operations emulated by two scalar ones.
 //
 // Reference semantics reproduced (file:line under /root/reference/pkg/src/fermatpath):
 //   embed / segments / clamped norms / gradient   batching.py:83-120
@@ -21,13 +33,102 @@
 
 namespace fp {
 
+// ---- paired arithmetic -------------------------------------------------------
+template <typename R> struct PairOf;
+template <> struct PairOf<float> { using T = float2; };
+template <> struct PairOf<double> { using T = double2; };
+template <typename R> using V2 = typename PairOf<R>::T;
+
+__device__ __forceinline__ float2 mk2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ double2 mk2(double a, double b) { return make_double2(a, b); }
+template <typename R>
+__device__ __forceinline__ V2<R> bc2(R a) { return mk2(a, a); }
+
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+// Products are FFMA2 with a -0 addend that ptxas cannot see (`nz`, a kernel
+// argument): ptxas contracts FMUL2 + FADD2 into FFMA2 even under -fmad=false,
+// which would round differently in different kernels. a * b + (-0) == a * b
+// exactly, so each lane still rounds like the scalar product.
+__device__ __forceinline__ float2 mulz(float2 a, float2 b, float nz) {
+  return __ffma2_rn(a, b, make_float2(nz, nz));
+}
+// Plain FMUL2, only where the product feeds an FFMA2 addend (nothing to contract).
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 neg2(float2 a) { return make_float2(-a.x, -a.y); }
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) { return __fadd2_rn(a, neg2(b)); }
+
+__device__ __forceinline__ double2 fma2(double2 a, double2 b, double2 c) {
+  return make_double2(fma(a.x, b.x, c.x), fma(a.y, b.y, c.y));
+}
+__device__ __forceinline__ double2 mulz(double2 a, double2 b, double) {
+  return make_double2(a.x * b.x, a.y * b.y);
+}
+__device__ __forceinline__ double2 mul2(double2 a, double2 b) { return make_double2(a.x * b.x, a.y * b.y); }
+__device__ __forceinline__ double2 add2(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 neg2(double2 a) { return make_double2(-a.x, -a.y); }
+__device__ __forceinline__ double2 sub2(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+
+template <typename P>
+__device__ __forceinline__ auto& lane(P& p, int h) { return h ? p.y : p.x; }
+template <typename P>
+__device__ __forceinline__ auto lane(const P& p, int h) { return h ? p.y : p.x; }
+
+// Vectors over the NA unknowns: NP pairs, element j in lane j & 1 of pair j >> 1.
+template <int NA>
+struct Packed {
+  static constexpr int NP = (NA + 1) / 2;  // pairs
+  static constexpr int NF = NA / 2;        // full pairs (no padding lane)
+};
+#define FP_EL(v, j) lane((v)[(j) >> 1], (j) & 1)
+
+// v . w over the NA real elements: lane-wise pair chains, then the two lanes
+// (and the unpaired last element of an odd NA).
+template <typename R, int NA>
+__device__ __forceinline__ R dotv(const V2<R> (&a)[Packed<NA>::NP], const V2<R> (&b)[Packed<NA>::NP], R nz) {
+  constexpr int NF = Packed<NA>::NF;
+  R r;
+  if constexpr (NF > 0) {
+    V2<R> acc = NF > 1 ? mul2(a[0], b[0]) : mulz(a[0], b[0], nz);
+#pragma unroll
+    for (int m = 1; m < NF; ++m) acc = fma2(a[m], b[m], acc);
+    r = acc.x + acc.y;
+    if constexpr (NA & 1) r = fma(a[NF].x, b[NF].x, r);
+  } else {
+    r = a[0].x * b[0].x;
+  }
+  return r;
+}
+
+// max_j |v_j| over the real elements, NaN-propagating (ALU pipe).
+template <typename R, int NA>
+__device__ __forceinline__ R absmaxv(const V2<R> (&a)[Packed<NA>::NP]) {
+  R m = fabs(a[0].x);
+#pragma unroll
+  for (int j = 1; j < NA; ++j) m = absmax_nan(m, FP_EL(a, j));
+  return m;
+}
+
+// ---- geometry ----------------------------------------------------------------
 template <typename R, int K>
 struct Geo {
-  R A[K][3][2];  // basis, row r, column c
-  R b[K][3];     // anchor
-  R x0[3], xe[3];
-  R eps;         // 1e-12 (1 + |end - start|), fp64 then cast (batching.py:67-72)
-  R reps;        // 1 / eps
+  V2<R> Axy[K][2];  // basis column c of interaction i, rows x and y
+  R Az[K][2];       // basis column c, row z
+  V2<R> bxy[K];     // anchor rows x, y
+  R bz[K];
+  V2<R> x0xy, xexy;  // start / end
+  R x0z, xez;
+  R nz;    // -0, opaque to ptxas (see mulz); kernels set it from their argument
+  R eps;   // 1e-12 (1 + |end - start|), fp64 then cast (batching.py:67-72)
+  R reps;  // 1 / eps
+  __device__ __forceinline__ R A(int i, int r, int c) const {
+    return r == 0 ? Axy[i][c].x : (r == 1 ? Axy[i][c].y : Az[i][c]);
+  }
+  __device__ __forceinline__ R b(int i, int r) const {
+    return r == 0 ? bxy[i].x : (r == 1 ? bxy[i].y : bz[i]);
+  }
+  __device__ __forceinline__ R x0(int r) const { return r == 0 ? x0xy.x : (r == 1 ? x0xy.y : x0z); }
+  __device__ __forceinline__ R xe(int r) const { return r == 0 ? xexy.x : (r == 1 ? xexy.y : xez); }
 };
 
 // Load one path's geometry from a record in the reference layout.
@@ -38,36 +139,63 @@ __device__ __forceinline__ void load_geo(Geo<R, K>& G, const R* basis, const R* 
 #pragma unroll
   for (int i = 0; i < K; ++i) {
 #pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      G.A[i][r][0] = basis[i * 6 + r * 2 + 0];
-      G.A[i][r][1] = L::plane(i) ? basis[i * 6 + r * 2 + 1] : R(0);
-      G.b[i][r] = anchor[i * 3 + r];
+    for (int c = 0; c < 2; ++c) {
+      const bool live = c == 0 || L::plane(i);
+      G.Axy[i][c] = mk2(live ? basis[i * 6 + c] : R(0), live ? basis[i * 6 + 2 + c] : R(0));
+      G.Az[i][c] = live ? basis[i * 6 + 4 + c] : R(0);
     }
+    G.bxy[i] = mk2(anchor[i * 3 + 0], anchor[i * 3 + 1]);
+    G.bz[i] = anchor[i * 3 + 2];
   }
-#pragma unroll
-  for (int r = 0; r < 3; ++r) {
-    G.x0[r] = start[r];
-    G.xe[r] = end[r];
-  }
-  const double dx = double(G.xe[0]) - double(G.x0[0]);
-  const double dy = double(G.xe[1]) - double(G.x0[1]);
-  const double dz = double(G.xe[2]) - double(G.x0[2]);
+  G.x0xy = mk2(start[0], start[1]);
+  G.x0z = start[2];
+  G.xexy = mk2(end[0], end[1]);
+  G.xez = end[2];
+  const double dx = double(end[0]) - double(start[0]);
+  const double dy = double(end[1]) - double(start[1]);
+  const double dz = double(end[2]) - double(start[2]);
   const double nrm = __dsqrt_rn(__fma_rn(dz, dz, __fma_rn(dy, dy, dx * dx)));
   G.eps = R(1e-12 * (1.0 + nrm));
   G.reps = Num<R>::rcp(G.eps);
+  G.nz = R(-0.0);
 }
 
+// A_i v_i as (xy pair, z) for the unknowns (v0, v1) of interaction i.
+template <typename R, int K, bool PLANE>
+__device__ __forceinline__ void apply_A(const Geo<R, K>& G, int i, R v0, R v1, V2<R>& xy, R& z) {
+  xy = PLANE ? mul2(G.Axy[i][0], bc2(v0)) : mulz(G.Axy[i][0], bc2(v0), G.nz);
+  z = G.Az[i][0] * v0;
+  if (PLANE) {
+    xy = fma2(G.Axy[i][1], bc2(v1), xy);
+    z = fma(G.Az[i][1], v1, z);
+  }
+}
+
+// ---- per-path state -------------------------------------------------------------
 template <typename R, int K, unsigned MASK>
 struct PathState {
   using L = Lay<K, MASK>;
   static constexpr int S = L::S;
   static constexpr int NA = L::NA;
+  static constexpr int NP = Packed<NA>::NP;
 
-  R t[NA];     // active unknowns
-  R g[NA];     // clamped-norm gradient at t
-  R s[S][3];   // segments at t
-  R rn[S];     // 1 / max(|s_k|, eps)
-  R nu[S];     // |s_k| (unclamped)
+  V2<R> t[NP];    // active unknowns
+  V2<R> g[NP];    // clamped-norm gradient at t
+  V2<R> sxy[S];   // segments at t (x, y)
+  R sz[S];        //                (z)
+  R rn[S];        // 1 / max(|s_k|, eps)
+  R nu[S];        // |s_k| (unclamped; valid after eval<false> / finish_norms)
+
+  __device__ __forceinline__ R& T(int j) { return FP_EL(t, j); }
+  __device__ __forceinline__ R T(int j) const { return FP_EL(t, j); }
+  __device__ __forceinline__ R Gr(int j) const { return FP_EL(g, j); }
+  __device__ __forceinline__ R S3(int k, int r) const {
+    return r == 0 ? sxy[k].x : (r == 1 ? sxy[k].y : sz[k]);
+  }
+  __device__ __forceinline__ void zero_t() {
+#pragma unroll
+    for (int m = 0; m < NP; ++m) t[m] = mk2(R(0), R(0));
+  }
 
   // Path length: sum of unclamped norms (batching.py:123-126).
   __device__ __forceinline__ R length() const {
@@ -84,49 +212,87 @@ struct PathState {
     return m;
   }
 
-  // x_i = A_i t_i + b_i (geometry.py:153-165)
-  __device__ __forceinline__ void points(const Geo<R, K>& G, R (&P)[K + 2][3]) const {
-#pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      P[0][r] = G.x0[r];
-      P[K + 1][r] = G.xe[r];
-    }
+  // x_i = A_i t_i + b_i (geometry.py:153-165); index 0 / K+1 are start / end.
+  // The dense layout's inert term 0 * t_i1 adds an exact zero, so every
+  // kernel embeds a path identically.
+  __device__ __forceinline__ void points(const Geo<R, K>& G, V2<R> (&Pxy)[K + 2], R (&Pz)[K + 2]) const {
+    Pxy[0] = G.x0xy;
+    Pz[0] = G.x0z;
+    Pxy[K + 1] = G.xexy;
+    Pz[K + 1] = G.xez;
 #pragma unroll
     for (int i = 0; i < K; ++i) {
-#pragma unroll
-      for (int r = 0; r < 3; ++r) {
-        R v = G.A[i][r][0] * t[L::idx(i, 0)];
-        if (L::plane(i)) v = fma(G.A[i][r][1], t[L::idx(i, 1)], v);
-        P[i + 1][r] = v + G.b[i][r];
+      // b_i + A_i0 t_i0 (+ A_i1 t_i1) as one explicit FMA chain
+      const R t0 = T(L::idx(i, 0));
+      Pxy[i + 1] = fma2(G.Axy[i][0], bc2(t0), G.bxy[i]);
+      Pz[i + 1] = fma(G.Az[i][0], t0, G.bz[i]);
+      if (L::plane(i)) {
+        const R t1 = T(L::idx(i, 1));
+        Pxy[i + 1] = fma2(G.Axy[i][1], bc2(t1), Pxy[i + 1]);
+        Pz[i + 1] = fma(G.Az[i][1], t1, Pz[i + 1]);
       }
     }
   }
 
+  // Points as plain 3-vectors (outputs).
+  __device__ __forceinline__ void points(const Geo<R, K>& G, R (&X)[K + 2][3]) const {
+    V2<R> Pxy[K + 2];
+    R Pz[K + 2];
+    points(G, Pxy, Pz);
+#pragma unroll
+    for (int i = 0; i < K + 2; ++i) {
+      X[i][0] = Pxy[i].x;
+      X[i][1] = Pxy[i].y;
+      X[i][2] = Pz[i];
+    }
+  }
+
   // Embed, segments, norms, clamped gradient into `gout` (batching.py:95-104).
-  __device__ __forceinline__ void eval(const Geo<R, K>& G, R (&gout)[NA]) {
-    R P[K + 2][3];
-    points(G, P);
-    R u[S][3];
+  // LIGHT (the BFGS loop): reciprocal clamped norms only; the unclamped norms
+  // `nu` are left stale until finish_norms().
+  template <bool LIGHT = false>
+  __device__ __forceinline__ void eval(const Geo<R, K>& G, V2<R> (&gout)[NP]) {
+    V2<R> Pxy[K + 2];
+    R Pz[K + 2];
+    points(G, Pxy, Pz);
+    V2<R> uxy[S];
+    R uz[S];
 #pragma unroll
     for (int k = 0; k < S; ++k) {
-#pragma unroll
-      for (int r = 0; r < 3; ++r) s[k][r] = P[k + 1][r] - P[k][r];
-      R q = s[k][0] * s[k][0];
-      q = fma(s[k][1], s[k][1], q);
-      q = fma(s[k][2], s[k][2], q);
-      R nc;
-      norm_rcp(q, G.eps, G.reps, nu[k], nc, rn[k]);
-#pragma unroll
-      for (int r = 0; r < 3; ++r) u[k][r] = s[k][r] * rn[k];
+      sxy[k] = sub2(Pxy[k + 1], Pxy[k]);
+      sz[k] = Pz[k + 1] - Pz[k];
+      R q = sxy[k].x * sxy[k].x;
+      q = fma(sxy[k].y, sxy[k].y, q);
+      q = fma(sz[k], sz[k], q);
+      if (LIGHT) {
+        rcp_norm(q, G.eps, G.reps, rn[k]);
+      } else {
+        R nc;
+        norm_rcp(q, G.eps, G.reps, nu[k], nc, rn[k]);
+      }
+      uxy[k] = mulz(sxy[k], bc2(rn[k]), G.nz);
+      uz[k] = sz[k] * rn[k];
     }
+    if constexpr (NA & 1) gout[NP - 1].y = R(0);
 #pragma unroll
     for (int i = 0; i < K; ++i) {
-      const R q0 = u[i][0] - u[i + 1][0];
-      const R q1 = u[i][1] - u[i + 1][1];
-      const R q2 = u[i][2] - u[i + 1][2];
-      gout[L::idx(i, 0)] = fma(G.A[i][2][0], q2, fma(G.A[i][1][0], q1, G.A[i][0][0] * q0));
+      const V2<R> qxy = sub2(uxy[i], uxy[i + 1]);
+      const R qz = uz[i] - uz[i + 1];
+      FP_EL(gout, L::idx(i, 0)) = fma(G.Az[i][0], qz, fma(G.Axy[i][0].y, qxy.y, G.Axy[i][0].x * qxy.x));
       if (L::plane(i))
-        gout[L::idx(i, 1)] = fma(G.A[i][2][1], q2, fma(G.A[i][1][1], q1, G.A[i][0][1] * q0));
+        FP_EL(gout, L::idx(i, 1)) = fma(G.Az[i][1], qz, fma(G.Axy[i][1].y, qxy.y, G.Axy[i][1].x * qxy.x));
+    }
+  }
+
+  // Unclamped norms of the current segments (bitwise those eval<false> gives).
+  __device__ __forceinline__ void finish_norms(const Geo<R, K>& G) {
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      R q = sxy[k].x * sxy[k].x;
+      q = fma(sxy[k].y, sxy[k].y, q);
+      q = fma(sz[k], sz[k], q);
+      R nc, r;
+      norm_rcp(q, G.eps, G.reps, nu[k], nc, r);
     }
   }
 
@@ -134,35 +300,34 @@ struct PathState {
   // `zero` when the direction moves no interaction point. The first fixed-
   // point iterate starts at alpha = 0, where the trial segments are exactly
   // the current ones, so it reuses their clamped norms.
-  __device__ __forceinline__ R step_size(const Geo<R, K>& G, const R (&p)[NA], int fp_iters,
+  __device__ __forceinline__ R step_size(const Geo<R, K>& G, const V2<R> (&p)[NP], int fp_iters,
                                          bool& zero) const {
-    R w[K][3];
+    V2<R> wxy[K];
+    R wz[K];
 #pragma unroll
     for (int i = 0; i < K; ++i) {
-#pragma unroll
-      for (int r = 0; r < 3; ++r) {
-        R v = G.A[i][r][0] * p[L::idx(i, 0)];
-        if (L::plane(i)) v = fma(G.A[i][r][1], p[L::idx(i, 1)], v);
-        w[i][r] = v;
-      }
+      if (L::plane(i))
+        apply_A<R, K, true>(G, i, FP_EL(p, L::idx(i, 0)), FP_EL(p, L::idx(i, 1)), wxy[i], wz[i]);
+      else
+        apply_A<R, K, false>(G, i, FP_EL(p, L::idx(i, 0)), R(0), wxy[i], wz[i]);
     }
-    R d[S][3];
-#pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      d[0][r] = w[0][r];
-      d[K][r] = -w[K - 1][r];
-    }
+    V2<R> dxy[S];
+    R dz[S];
+    dxy[0] = wxy[0];
+    dz[0] = wz[0];
+    dxy[K] = neg2(wxy[K - 1]);
+    dz[K] = -wz[K - 1];
 #pragma unroll
     for (int k = 1; k < K; ++k) {
-#pragma unroll
-      for (int r = 0; r < 3; ++r) d[k][r] = w[k][r] - w[k - 1][r];
+      dxy[k] = sub2(wxy[k], wxy[k - 1]);
+      dz[k] = wz[k] - wz[k - 1];
     }
     R a2[S], c[S];
     R total;
 #pragma unroll
     for (int k = 0; k < S; ++k) {
-      a2[k] = fma(d[k][2], d[k][2], fma(d[k][1], d[k][1], d[k][0] * d[k][0]));
-      c[k] = fma(d[k][2], s[k][2], fma(d[k][1], s[k][1], d[k][0] * s[k][0]));
+      a2[k] = fma(dz[k], dz[k], fma(dxy[k].y, dxy[k].y, dxy[k].x * dxy[k].x));
+      c[k] = fma(dz[k], sz[k], fma(dxy[k].y, sxy[k].y, dxy[k].x * sxy[k].x));
       total = k == 0 ? a2[0] : total + a2[k];
     }
     zero = total <= Num<R>::tiny();
@@ -181,11 +346,10 @@ struct PathState {
       R num = R(0), den = R(0);
 #pragma unroll
       for (int k = 0; k < S; ++k) {
-        const R e0 = fma(alpha, d[k][0], s[k][0]);
-        const R e1 = fma(alpha, d[k][1], s[k][1]);
-        const R e2 = fma(alpha, d[k][2], s[k][2]);
+        const V2<R> exy = fma2(bc2(alpha), dxy[k], sxy[k]);
+        const R e2 = fma(alpha, dz[k], sz[k]);
         R n0, n, ri;
-        norm_rcp(fma(e2, e2, fma(e1, e1, e0 * e0)), G.eps, G.reps, n0, n, ri);
+        norm_rcp(fma(e2, e2, fma(exy.y, exy.y, exy.x * exy.x)), G.eps, G.reps, n0, n, ri);
         num = k == 0 ? c[0] * ri : fma(c[k], ri, num);
         den = k == 0 ? a2[0] * ri : fma(a2[k], ri, den);
       }
@@ -196,33 +360,16 @@ struct PathState {
   }
 };
 
-// Dot product over the active unknowns as two FMA chains, one per basis
-// column c (half the dependent latency of one chain). Grouping by column, not
-// by compressed position, keeps the kind-specialised kernels bit-identical to
-// the dense one: an edge's inert term only adds an exact zero to chain 1.
-template <typename R, int K, unsigned MASK, int NA>
-__device__ __forceinline__ R dot(const R (&a)[NA], const R (&b)[NA]) {
-  using L = Lay<K, MASK>;
-  R c0 = a[L::idx(0, 0)] * b[L::idx(0, 0)];
-#pragma unroll
-  for (int i = 1; i < K; ++i) c0 = fma(a[L::idx(i, 0)], b[L::idx(i, 0)], c0);
-  bool any = false;
-  R c1 = R(0);
-#pragma unroll
-  for (int i = 0; i < K; ++i) {
-    if (!L::plane(i)) continue;
-    c1 = any ? fma(a[L::idx(i, 1)], b[L::idx(i, 1)], c1) : a[L::idx(i, 1)] * b[L::idx(i, 1)];
-    any = true;
-  }
-  return any ? c0 + c1 : c0;
-}
-
 // Packed symmetric inverse-Hessian approximation with the BFGS update.
+//
+// Storage: row pairs. Pair (m, c), c >= 2m, holds {h(2m, c), h(2m+1, c)};
+// the diagonal block's h(2m+1, 2m) duplicates h(2m, 2m+1) and is kept equal
+// to it. Odd NA: the last pair's hi lane is a padding row (never read).
 //
 // The reference update (solver.py:180-199)
 //   H' = H - rho (s Hy^T + Hy s^T) + (rho^2 yHy + rho) s s^T
 // is applied in the equivalent symmetric two-term form H' = H + s z^T + z s^T
-// with z = -rho Hy + (rho^2 yHy + rho)/2 s (two FMAs per packed entry), and
+// with z = -rho Hy + (rho^2 yHy + rho)/2 s (two FFMA2 per stored pair), and
 // the next direction -H' g_new is obtained from H g_new by the same rank-two
 // formula, so each iteration needs one matrix-vector product: H y follows
 // from H g_new + p (p = -H g_old).
@@ -230,73 +377,90 @@ template <typename R, int K, unsigned MASK>
 struct InvHess {
   using L = Lay<K, MASK>;
   static constexpr int NA = L::NA;
-  static constexpr int NH = NA * (NA + 1) / 2;
-  R h[NH];
+  static constexpr int NP = Packed<NA>::NP;
+  static constexpr int NHP = NP * NA - NP * (NP - 1);  // sum over m of (NA - 2m)
+  V2<R> h[NHP];
   R bound;  // upper bound on max |h_ij| (for the overflow pre-check)
 
-  __device__ static constexpr int id(int i, int j) {
-    return i <= j ? i * NA - i * (i - 1) / 2 + (j - i) : j * NA - j * (j - 1) / 2 + (i - j);
+  __device__ static constexpr int off(int m) { return m * NA - m * (m - 1); }
+  __device__ static constexpr int pid(int m, int c) { return off(m) + c - 2 * m; }
+  // h(r, c) for any r, c (symmetric)
+  __device__ __forceinline__ R get(int r, int c) const {
+    return r <= c ? lane(h[pid(r >> 1, c)], r & 1) : lane(h[pid(c >> 1, r)], c & 1);
   }
+
   __device__ __forceinline__ void identity() {
 #pragma unroll
-    for (int i = 0; i < NA; ++i)
+    for (int m = 0; m < NP; ++m)
 #pragma unroll
-      for (int j = i; j < NA; ++j) h[id(i, j)] = i == j ? R(1) : R(0);
+      for (int c = 2 * m; c < NA; ++c)
+        h[pid(m, c)] = mk2(c == 2 * m ? R(1) : R(0), c == 2 * m + 1 ? R(1) : R(0));
     bound = R(1);
   }
-  // out = H v, each row as the column-grouped two-chain dot product.
-  __device__ __forceinline__ void mul(const R (&v)[NA], R (&out)[NA]) const {
+  // out = H v. Row pair m: the columns c < 2m come from the stored pairs of
+  // the earlier row pairs (dot of {h(2m', c), h(2m'+1, c)} with {v_2m', v_2m'+1}),
+  // then the pair chain over c >= 2m continues from them.
+  __device__ __forceinline__ void mul(const V2<R> (&v)[NP], V2<R> (&out)[NP], R nz) const {
 #pragma unroll
-    for (int r = 0; r < NA; ++r) {
-      R c0 = h[id(r, L::idx(0, 0))] * v[L::idx(0, 0)];
+    for (int m = 0; m < NP; ++m) {
+      V2<R> acc;
+      if (m == 0) {
+        acc = NA > 1 ? mul2(h[pid(0, 0)], bc2(v[0].x)) : mulz(h[pid(0, 0)], bc2(v[0].x), nz);
+      } else {
+        R lo[2];
 #pragma unroll
-      for (int i = 1; i < K; ++i) c0 = fma(h[id(r, L::idx(i, 0))], v[L::idx(i, 0)], c0);
-      bool any = false;
-      R c1 = R(0);
+        for (int e = 0; e < 2; ++e) {
+          const int c = 2 * m + e;
+          if (c >= NA) {
+            lo[e] = R(0);
+            continue;
+          }
+          V2<R> l = m > 1 ? mul2(h[pid(0, c)], v[0]) : mulz(h[pid(0, c)], v[0], nz);
 #pragma unroll
-      for (int i = 0; i < K; ++i) {
-        if (!L::plane(i)) continue;
-        const int j = L::idx(i, 1);
-        c1 = any ? fma(h[id(r, j)], v[j], c1) : h[id(r, j)] * v[j];
-        any = true;
+          for (int mm = 1; mm < m; ++mm) l = fma2(h[pid(mm, c)], v[mm], l);
+          lo[e] = l.x + l.y;
+        }
+        acc = fma2(h[pid(m, 2 * m)], bc2(v[m].x), mk2(lo[0], lo[1]));
       }
-      out[r] = any ? c0 + c1 : c0;
+#pragma unroll
+      for (int c = 2 * m + 1; c < NA; ++c) acc = fma2(h[pid(m, c)], bc2(FP_EL(v, c)), acc);
+      out[m] = acc;
     }
   }
   // One BFGS step. In: step sg, gradient change y, new gradient gn, old
-  // direction p (= -H g_old), curvature flag ok and sy = sg.y. Out: p =
-  // -H' gn with H' the updated matrix (or the old one when the update is
-  // skipped: failed curvature test or a non-finite H', solver.py:184,198).
-  __device__ __forceinline__ void step(const R (&sg)[NA], const R (&y)[NA], const R (&gn)[NA],
-                                       R (&p)[NA], bool ok, R sy) {
-    R Hg[NA];
-    mul(gn, Hg);
+  // direction p (= -H g_old), curvature flag ok, sy = sg.y and ms =
+  // max_j |sg_j|. Out: p = -H' gn with H' the updated matrix (or the old one
+  // when the update is skipped: failed curvature test or a non-finite H',
+  // solver.py:184,198).
+  __device__ __forceinline__ void step(const V2<R> (&sg)[NP], const V2<R> (&y)[NP],
+                                       const V2<R> (&gn)[NP], V2<R> (&p)[NP], bool ok, R sy, R ms,
+                                       R nz) {
+    V2<R> Hg[NP];
+    mul(gn, Hg, nz);
     if (ok) {
-      R Hy[NA];
+      V2<R> Hy[NP];
 #pragma unroll
-      for (int i = 0; i < NA; ++i) Hy[i] = Hg[i] + p[i];
+      for (int m = 0; m < NP; ++m) Hy[m] = add2(Hg[m], p[m]);
       const R rho = rcp_fast(sy);
-      const R yHy = dot<R, K, MASK, NA>(y, Hy);
+      const R yHy = dotv<R, NA>(y, Hy, nz);
       const R half = R(0.5) * fma(rho * rho, yHy, rho);
-      R z[NA];
-      R ss = R(0), sz = R(0);
+      V2<R> z[NP];
 #pragma unroll
-      for (int i = 0; i < NA; ++i) {
-        z[i] = fma(half, sg[i], -(rho * Hy[i]));
-        ss += fabs(sg[i]);
-        sz += fabs(z[i]);
-      }
-      // |H'_ij| <= bound + 2 sum|s| sum|z|; NaN/inf propagate into nb.
-      const R nb = fma(R(2) * ss, sz, bound) * R(1.0009765625);
+      for (int m = 0; m < NP; ++m) z[m] = fma2(bc2(half), sg[m], mul2(bc2(-rho), Hy[m]));
+      // |H'_ij| <= bound + |z_i s_j + s_i z_j| <= bound + 2 max|s| max|z|.
+      // The magnitudes are FMNMX (ALU pipe) reductions; NaN/inf propagate
+      // into nb and send the update through the per-entry check.
+      const R mz = absmaxv<R, NA>(z);
+      const R nb = fma(R(2) * ms, mz, bound) * R(1.0009765625);
       bool take = true;
       if (!(nb < R(1e36))) {
         // Rare: possible overflow. Check every entry before committing.
         R mx = R(0);
 #pragma unroll
-        for (int i = 0; i < NA; ++i)
+        for (int r = 0; r < NA; ++r)
 #pragma unroll
-          for (int j = i; j < NA; ++j) {
-            const R v = fma(z[i], sg[j], fma(sg[i], z[j], h[id(i, j)]));
+          for (int c = r; c < NA; ++c) {
+            const R v = fma(FP_EL(z, r), FP_EL(sg, c), fma(FP_EL(sg, r), FP_EL(z, c), get(r, c)));
             take = take && finite(v);
             mx = fabs(v) > mx ? fabs(v) : mx;
           }
@@ -306,29 +470,39 @@ struct InvHess {
       }
       if (take) {
 #pragma unroll
-        for (int i = 0; i < NA; ++i)
+        for (int m = 0; m < NP; ++m) {
 #pragma unroll
-          for (int j = i; j < NA; ++j) h[id(i, j)] = fma(z[i], sg[j], fma(sg[i], z[j], h[id(i, j)]));
-        const R zg = dot<R, K, MASK, NA>(z, gn), sgn = dot<R, K, MASK, NA>(sg, gn);
+          for (int c = 2 * m; c < NA; ++c)
+            h[pid(m, c)] = fma2(z[m], bc2(FP_EL(sg, c)), fma2(sg[m], bc2(FP_EL(z, c)), h[pid(m, c)]));
+          if (2 * m + 1 < NA) h[pid(m, 2 * m)].y = h[pid(m, 2 * m + 1)].x;  // keep H symmetric
+        }
+        const R zg = dotv<R, NA>(z, gn, nz), sgn = dotv<R, NA>(sg, gn, nz);
 #pragma unroll
-        for (int i = 0; i < NA; ++i) p[i] = -fma(sg[i], zg, fma(z[i], sgn, Hg[i]));
+        for (int m = 0; m < NP; ++m) p[m] = fma2(sg[m], bc2(-zg), fma2(z[m], bc2(-sgn), neg2(Hg[m])));
         return;
       }
     }
 #pragma unroll
-    for (int i = 0; i < NA; ++i) p[i] = -Hg[i];
+    for (int m = 0; m < NP; ++m) p[m] = neg2(Hg[m]);
   }
 };
 
-// Stationarity gate |g| < 1e-5 (1 + L) (implicit_diff.py:25,30-36).
+// |g|^2 as one sequential chain in coordinate order: the dense 2K layout only
+// adds exact zeros for inert coordinates, so every kernel (dense, specialised,
+// VJP-only) classifies a path identically.
 template <typename R, int NA>
-__device__ __forceinline__ bool stationary(const R (&g)[NA], R len) {
+__device__ __forceinline__ R norm2_seq(const V2<R> (&g)[Packed<NA>::NP]) {
   R q = R(0);
 #pragma unroll
-  for (int i = 0; i < NA; ++i) q = fma(g[i], g[i], q);
-  return Num<R>::sqrt_(q) < R(1e-5) * (R(1) + len);
+  for (int j = 0; j < NA; ++j) q = fma(FP_EL(g, j), FP_EL(g, j), q);
+  return q;
 }
 
+// Stationarity gate |g| < 1e-5 (1 + L) (implicit_diff.py:25,30-36).
+template <typename R, int NA>
+__device__ __forceinline__ bool stationary(const V2<R> (&g)[Packed<NA>::NP], R len) {
+  return Num<R>::sqrt_(norm2_seq<R, NA>(g)) < R(1e-5) * (R(1) + len);
+}
 
 // The fixed-iteration BFGS loop (solver.py:146-215) from the state P (which
 // must hold t and its evaluation). Returns DEGENERATE_ENTRY / ZERO_DIRECTION
@@ -341,43 +515,51 @@ __device__ __forceinline__ uint8_t bfgs_solve(const Geo<R, K>& G, PathState<R, K
                                               R* H_out) {
   using L = Lay<K, MASK>;
   constexpr int NA = L::NA;
+  constexpr int NP = Packed<NA>::NP;
   uint8_t st = 0;
   if (P.min_norm() <= G.eps) st |= FP_STATUS_DEGENERATE_ENTRY;  // checked_segments (solver.py:166)
   InvHess<R, K, MASK> H;
   H.identity();
-  R p[NA];
+  V2<R> p[NP];
 #pragma unroll
-  for (int j = 0; j < NA; ++j) p[j] = -P.g[j];  // H = I
+  for (int m = 0; m < NP; ++m) p[m] = neg2(P.g[m]);  // H = I
   for (int it = 0; it < iterations; ++it) {
     bool zero;
     const R alpha = P.step_size(G, p, fp_iters, zero);
     if (zero) st |= FP_STATUS_ZERO_DIRECTION;
-    R sg[NA];
+    V2<R> sg[NP];
 #pragma unroll
-    for (int j = 0; j < NA; ++j) {
-      sg[j] = alpha * p[j];
-      P.t[j] = P.t[j] + sg[j];
+    for (int m = 0; m < NP; ++m) {
+      sg[m] = mulz(bc2(alpha), p[m], G.nz);
+      P.t[m] = add2(P.t[m], sg[m]);
     }
-    R gn[NA];
-    P.eval(G, gn);
-    R y[NA];
+    V2<R> gn[NP];
+    P.template eval<true>(G, gn);
+    V2<R> y[NP];
 #pragma unroll
-    for (int j = 0; j < NA; ++j) y[j] = gn[j] - P.g[j];
-    const R sy = dot<R, K, MASK, NA>(sg, y);
-    const R ss = dot<R, K, MASK, NA>(sg, sg);
-    const R yy = dot<R, K, MASK, NA>(y, y);
-    const bool ok = sy > (R(1e-12) * sqrt_test(ss)) * sqrt_test(yy);
-    H.step(sg, y, gn, p, ok, sy);
+    for (int m = 0; m < NP; ++m) y[m] = sub2(gn[m], P.g[m]);
+    // Curvature test sy > 1e-12 |s| |y| (solver.py:184). |s| |y| <= NA
+    // max|s_j| max|y_j|, so a sy above that bound (the common case) passes
+    // without the two norms; sy <= 0 (or NaN) fails; only the band between
+    // evaluates the reference's test with the norms.
+    const R sy = dotv<R, NA>(sg, y, G.nz);
+    const R ms = absmaxv<R, NA>(sg), my = absmaxv<R, NA>(y);
+    bool ok = sy > (R(1e-12 * NA * 1.0009765625) * ms) * my;
+    if (!ok && sy > R(0)) {
+      const R ss = dotv<R, NA>(sg, sg, G.nz);
+      const R yy = dotv<R, NA>(y, y, G.nz);
+      ok = sy > (R(1e-12) * sqrt_test(ss)) * sqrt_test(yy);
+    }
+    H.step(sg, y, gn, p, ok, sy, ms, G.nz);
 #pragma unroll
-    for (int j = 0; j < NA; ++j) P.g[j] = gn[j];
+    for (int m = 0; m < NP; ++m) P.g[m] = gn[m];
     if (trace_len != nullptr) {
-      R q = R(0);
-#pragma unroll
-      for (int j = 0; j < NA; ++j) q = fma(P.g[j], P.g[j], q);
+      P.finish_norms(G);
       trace_len[int64_t(it) * trace_ld + row] = P.length();
-      trace_gnorm[int64_t(it) * trace_ld + row] = Num<R>::sqrt_(q);
+      trace_gnorm[int64_t(it) * trace_ld + row] = Num<R>::sqrt_(norm2_seq<R, NA>(P.g));
     }
   }
+  P.finish_norms(G);
   if (H_out != nullptr) {
     R* Ho = H_out + row * (4 * K * K);
 #pragma unroll
@@ -387,7 +569,7 @@ __device__ __forceinline__ uint8_t bfgs_solve(const Geo<R, K>& G, PathState<R, K
         const int ii = i >> 1, ci = i & 1, jj = j >> 1, cj = j & 1;
         const bool ai = ci == 0 || L::plane(ii), aj = cj == 0 || L::plane(jj);
         R v = (i == j) ? R(1) : R(0);
-        if (ai && aj) v = H.h[InvHess<R, K, MASK>::id(L::idx(ii, ci), L::idx(jj, cj))];
+        if (ai && aj) v = H.get(L::idx(ii, ci), L::idx(jj, cj));
         Ho[i * 2 * K + j] = v;
       }
   }
@@ -406,7 +588,7 @@ __device__ __forceinline__ uint8_t final_status(const Geo<R, K>& G, const PathSt
   if (nmin < R(1e-3)) st |= FP_STATUS_SHORT_SEGMENT;
   bool fin = finite(len);
 #pragma unroll
-  for (int j = 0; j < NA; ++j) fin = fin && finite(P.t[j]) && finite(P.g[j]);
+  for (int j = 0; j < NA; ++j) fin = fin && finite(P.T(j)) && finite(P.Gr(j));
   if (!fin) st |= FP_STATUS_NONFINITE;
   return st;
 }
@@ -439,13 +621,13 @@ __device__ __forceinline__ uint8_t implicit_vjp(const Geo<R, K>& G, const PathSt
   for (int i = 0; i < K; ++i) {
 #pragma unroll
     for (int c = 0; c < 2; ++c)
-      act[i][c] = (G.A[i][0][c] != R(0)) || (G.A[i][1][c] != R(0)) || (G.A[i][2][c] != R(0));
+      act[i][c] = (G.A(i, 0, c) != R(0)) || (G.A(i, 1, c) != R(0)) || (G.A(i, 2, c) != R(0));
   }
   R u[S][3];
 #pragma unroll
   for (int k = 0; k < S; ++k)
 #pragma unroll
-    for (int r = 0; r < 3; ++r) u[k][r] = P.s[k][r] * P.rn[k];
+    for (int r = 0; r < 3; ++r) u[k][r] = P.S3(k, r) * P.rn[k];
   R q[K][3];
 #pragma unroll
   for (int i = 0; i < K; ++i)
@@ -470,18 +652,18 @@ __device__ __forceinline__ uint8_t implicit_vjp(const Geo<R, K>& G, const PathSt
     for (int i = 0; i < K; ++i)
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        au_in[i][c] = fma(G.A[i][2][c], u[i][2], fma(G.A[i][1][c], u[i][1], G.A[i][0][c] * u[i][0]));
+        au_in[i][c] = fma(G.A(i, 2, c), u[i][2], fma(G.A(i, 1, c), u[i][1], G.A(i, 0, c) * u[i][0]));
         au_out[i][c] =
-            fma(G.A[i][2][c], u[i + 1][2], fma(G.A[i][1][c], u[i + 1][1], G.A[i][0][c] * u[i + 1][0]));
+            fma(G.A(i, 2, c), u[i + 1][2], fma(G.A(i, 1, c), u[i + 1][1], G.A(i, 0, c) * u[i + 1][0]));
       }
     R rhs[K][2];
     R trace = R(0);
 #pragma unroll
     for (int i = 0; i < K; ++i) {
       R gii[3];
-      gii[0] = fma(G.A[i][2][0], G.A[i][2][0], fma(G.A[i][1][0], G.A[i][1][0], G.A[i][0][0] * G.A[i][0][0]));
-      gii[1] = fma(G.A[i][2][0], G.A[i][2][1], fma(G.A[i][1][0], G.A[i][1][1], G.A[i][0][0] * G.A[i][0][1]));
-      gii[2] = fma(G.A[i][2][1], G.A[i][2][1], fma(G.A[i][1][1], G.A[i][1][1], G.A[i][0][1] * G.A[i][0][1]));
+      gii[0] = fma(G.A(i, 2, 0), G.A(i, 2, 0), fma(G.A(i, 1, 0), G.A(i, 1, 0), G.A(i, 0, 0) * G.A(i, 0, 0)));
+      gii[1] = fma(G.A(i, 2, 0), G.A(i, 2, 1), fma(G.A(i, 1, 0), G.A(i, 1, 1), G.A(i, 0, 0) * G.A(i, 0, 1)));
+      gii[2] = fma(G.A(i, 2, 1), G.A(i, 2, 1), fma(G.A(i, 1, 1), G.A(i, 1, 1), G.A(i, 0, 1) * G.A(i, 0, 1)));
       const R ri = P.rn[i], ro = P.rn[i + 1];
       D[i][0] = (gii[0] - au_in[i][0] * au_in[i][0]) * ri + (gii[0] - au_out[i][0] * au_out[i][0]) * ro;
       D[i][1] = (gii[1] - au_in[i][0] * au_in[i][1]) * ri + (gii[1] - au_out[i][0] * au_out[i][1]) * ro;
@@ -491,15 +673,15 @@ __device__ __forceinline__ uint8_t implicit_vjp(const Geo<R, K>& G, const PathSt
         for (int a = 0; a < 2; ++a)
 #pragma unroll
           for (int b = 0; b < 2; ++b) {
-            const R gij = fma(G.A[i][2][a], G.A[i + 1][2][b],
-                              fma(G.A[i][1][a], G.A[i + 1][1][b], G.A[i][0][a] * G.A[i + 1][0][b]));
+            const R gij = fma(G.A(i, 2, a), G.A(i + 1, 2, b),
+                              fma(G.A(i, 1, a), G.A(i + 1, 1, b), G.A(i, 0, a) * G.A(i + 1, 0, b)));
             O[i][a][b] = -(gij - au_out[i][a] * au_in[i + 1][b]) * ro;
           }
       }
       // rhs = -(wl g + vT) on active coordinates, 0 on inert ones
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        const R gc = (c == 0 || L::plane(i)) ? P.g[L::idx(i, c)] : R(0);
+        const R gc = (c == 0 || L::plane(i)) ? P.Gr(L::idx(i, c)) : R(0);
         const R vc = vf[i][c];
         const R v = full ? fma(wl, gc, vc) : vc;
         rhs[i][c] = act[i][c] ? -v : R(0);
@@ -579,7 +761,7 @@ __device__ __forceinline__ uint8_t implicit_vjp(const Geo<R, K>& G, const PathSt
 #pragma unroll
   for (int i = 0; i < K; ++i)
 #pragma unroll
-    for (int r = 0; r < 3; ++r) dx[i][r] = fma(G.A[i][r][1], sol[i][1], G.A[i][r][0] * sol[i][0]);
+    for (int r = 0; r < 3; ++r) dx[i][r] = fma(G.A(i, r, 1), sol[i][1], G.A(i, r, 0) * sol[i][0]);
   R w[S][3];
 #pragma unroll
   for (int k = 0; k < S; ++k) {
