@@ -572,7 +572,7 @@ def main(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="tiny CPU samples (debugging)")
-    ap.add_argument("--policy", choices=("auto", "dense", "serial"), default="auto",
+    ap.add_argument("--policy", choices=("auto", "dense", "serial", "bucket", "tile"), default="auto",
                     help="kernel selection (fp_set_kernel_policy)")
     ap.add_argument("--workload", choices=("config1", "config2", "config3", "config4"),
                     default="config2")

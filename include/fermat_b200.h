@@ -196,15 +196,27 @@ int fp_image_method_f64(const double* basis, const double* anchor, const double*
 int fp_peak_ffma(int blocks, int iters, float* out, void* stream);
 
 /* ---- bookkeeping ---------------------------------------------------------- */
-/* Kernel selection: FP_POLICY_AUTO (default) buckets fp32 batches of order
- * <= 5 by interaction-kind mask on the device and runs kernels that carry
- * only the active unknowns; FP_POLICY_DENSE always runs the uniform 2K
- * kernel (identical results, used by the tests to prove it). */
+/* Kernel selection for fp32 solves / fused steps (other calls run the dense
+ * kernels). Every policy runs, for each path, the kernel variant carrying only
+ * its active unknowns (its interaction-kind mask), except FP_POLICY_DENSE.
+ *   FP_POLICY_AUTO (default): order <= 3 runs the tile kernel (one launch; each
+ *     warp dispatches on its paths' masks; no host round trip) unless the last
+ *     call of that order saw more than 1/8 mixed-mask warps (a scattered
+ *     layout), which then goes to the bucketed path; orders 4-5 are bucketed.
+ *   FP_POLICY_DENSE: the uniform 2K kernel for every path (agrees with the
+ *     specialised variants to rounding; used by the tests).
+ *   FP_POLICY_AUTO_SERIAL: bucketed, per-mask kernels one after another on
+ *     the caller's stream instead of concurrent side streams.
+ *   FP_POLICY_BUCKET: always bucketed (classify on the device, one host
+ *     round trip, one kernel per mask over its row range or permutation).
+ *   FP_POLICY_TILE: always the tile kernel for order <= 3.
+ * A path's results are bitwise the same under AUTO, AUTO_SERIAL, BUCKET and
+ * TILE. */
 #define FP_POLICY_AUTO 0
 #define FP_POLICY_DENSE 1
-/* as AUTO, but the per-mask kernels run one after another on the caller's
- * stream instead of on concurrent side streams */
 #define FP_POLICY_AUTO_SERIAL 2
+#define FP_POLICY_BUCKET 3
+#define FP_POLICY_TILE 4
 int fp_set_kernel_policy(int policy);
 
 /* Number of kernels this library has launched in the process (monotone). */

@@ -131,11 +131,14 @@ def check(rc: int, what: str) -> None:
 POLICY_AUTO = 0
 POLICY_DENSE = 1
 POLICY_AUTO_SERIAL = 2
+POLICY_BUCKET = 3
+POLICY_TILE = 4
 
 
 def set_kernel_policy(policy: str) -> None:
     """'auto' (kind-mask specialised kernels, default) or 'dense' (uniform 2K kernel)."""
-    code = {"auto": POLICY_AUTO, "dense": POLICY_DENSE, "serial": POLICY_AUTO_SERIAL}[policy]
+    code = {"auto": POLICY_AUTO, "dense": POLICY_DENSE, "serial": POLICY_AUTO_SERIAL,
+            "bucket": POLICY_BUCKET, "tile": POLICY_TILE}[policy]
     check(load().fp_set_kernel_policy(code), "fp_set_kernel_policy")
 
 

@@ -28,6 +28,7 @@ OBJ_DIR = os.path.join(REPO, "build", "obj")
 
 ORDERS = range(1, 9)
 SPECIALISED_MAX_ORDER = 5  # fp_bucket.h kMaxSpecialisedOrder
+TILE_MAX_ORDER = 3  # fp_abi.cu kMaxTileOrder (every mask inlined in one kernel)
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo", "-fmad=false", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
@@ -60,6 +61,8 @@ def _units(orders=ORDERS, obj_dir=None):
     inst = os.path.join(CSRC, "fp_inst.cu")
     for k in orders:
         parts = (0, 1, 2) if k <= SPECIALISED_MAX_ORDER else (0,)
+        if k <= TILE_MAX_ORDER:
+            parts += (3,)
         for part in parts:
             units.append((inst, os.path.join(obj_dir, f"fp_inst_k{k}_p{part}.o"),
                           [f"-DFP_INST_K={k}", f"-DFP_INST_PART={part}"]))
@@ -68,7 +71,8 @@ def _units(orders=ORDERS, obj_dir=None):
         if os.path.exists(path):
             units.append((path, os.path.join(obj_dir, extra.replace(".cu", ".o")), []))
     # longest units first so the parallel build finishes sooner
-    units.sort(key=lambda u: -sum(int(d.split("=")[1]) for d in u[2] if "FP_INST_K" in d))
+    units.sort(key=lambda u: -sum(int(d.split("=")[1]) * (4 if "FP_INST_PART=3" in " ".join(u[2]) else 1)
+                                  for d in u[2] if "FP_INST_K" in d))
     return units
 
 
@@ -129,6 +133,9 @@ def build_variant(out: str, orders, defines=(), jobs=None) -> str:
                 continue
             for R in ("float", "double"):
                 fh.write(f"template <> cudaError_t dispatch_dense<{R}, {k}>(const PathArgs<{R}>&, int, "
+                         "cudaStream_t) { return cudaErrorNotSupported; }\n")
+            if k <= TILE_MAX_ORDER:
+                fh.write(f"template <> cudaError_t dispatch_tile<{k}>(const PathArgs<float>&, int, "
                          "cudaStream_t) { return cudaErrorNotSupported; }\n")
             if k <= SPECIALISED_MAX_ORDER:
                 for fn in ("dispatch_masked_solve", "dispatch_masked_solve_vjp"):

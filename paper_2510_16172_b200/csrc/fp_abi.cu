@@ -93,22 +93,101 @@ static cudaError_t masked_k(int K, const PathArgs<float>& a, int op, unsigned m,
   }
 }
 
-// fp32 solve / fused step for K <= 5: classify paths by kind mask on the
-// device, then one specialised kernel per non-empty mask — the staged TMA
-// kernel on the mask's row range when it is contiguous, the gathering kernel
-// over a row permutation otherwise — on side streams so tails overlap.
+// ---- tile kernels and their layout probe ------------------------------------
+// The tile kernel (order <= kMaxTileOrder) counts warps whose paths carry
+// different kind masks; that count comes back asynchronously (pinned copy +
+// event, read by a later call once the event has completed — no sync). The
+// bucketed path learns the same number from its classification. AUTO keeps
+// using the tile kernel while the last known mixed fraction is small.
+constexpr int kMaxTileOrder = 3;
+constexpr double kMaxMixedFraction = 0.125;
+
+struct LayoutProbe {
+  std::mutex mu;
+  bool init[kMaxTileOrder + 1] = {};
+  bool pending[kMaxTileOrder + 1] = {};
+  cudaEvent_t ev[kMaxTileOrder + 1];
+  unsigned long long* host = nullptr;  // pinned, one slot per order
+  int64_t warps[kMaxTileOrder + 1] = {};
+  double frac[kMaxTileOrder + 1] = {};
+};
+static LayoutProbe& probe() {
+  static LayoutProbe p;
+  return p;
+}
+
+static bool tile_preferred(int K) {
+  LayoutProbe& p = probe();
+  std::lock_guard<std::mutex> lk(p.mu);
+  if (p.pending[K] && cudaEventQuery(p.ev[K]) == cudaSuccess) {
+    p.frac[K] = p.warps[K] ? double(p.host[K]) / double(p.warps[K]) : 0.0;
+    p.pending[K] = false;
+  }
+  return p.frac[K] <= kMaxMixedFraction;
+}
+
+static void record_mixed_fraction(int K, int64_t mixed, int64_t B) {
+  if (K > kMaxTileOrder) return;
+  LayoutProbe& p = probe();
+  std::lock_guard<std::mutex> lk(p.mu);
+  p.frac[K] = B > 0 ? double(mixed) / double((B + 31) / 32) : 0.0;
+  p.pending[K] = false;
+}
+
+static cudaError_t run_tile(int K, const PathArgs<float>& a0, int op, cudaStream_t s) {
+  PathArgs<float> a = a0;
+  unsigned long long* dev = nullptr;
+  cudaError_t e = cudaMallocAsync(&dev, sizeof(unsigned long long), s);
+  if (e != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(dev, 0, sizeof(unsigned long long), s)) != cudaSuccess) return e;
+  a.mixed_warps = dev;
+  switch (K) {
+    case 1: e = dispatch_tile<1>(a, op, s); break;
+    case 2: e = dispatch_tile<2>(a, op, s); break;
+    default: e = dispatch_tile<3>(a, op, s); break;
+  }
+  count_launches(1);
+  if (e == cudaSuccess) {
+    LayoutProbe& p = probe();
+    std::lock_guard<std::mutex> lk(p.mu);
+    if (p.host == nullptr) e = cudaMallocHost(&p.host, sizeof(unsigned long long) * (kMaxTileOrder + 1));
+    if (e == cudaSuccess && !p.init[K]) {
+      e = cudaEventCreateWithFlags(&p.ev[K], cudaEventDisableTiming);
+      p.init[K] = e == cudaSuccess;
+    }
+    if (e == cudaSuccess && !p.pending[K]) {
+      e = cudaMemcpyAsync(p.host + K, dev, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
+      if (e == cudaSuccess) e = cudaEventRecord(p.ev[K], s);
+      p.warps[K] = (a.B - a.row_begin + 31) / 32;
+      p.pending[K] = e == cudaSuccess;
+    }
+  }
+  cudaError_t f = cudaFreeAsync(dev, s);
+  return e != cudaSuccess ? e : f;
+}
+
+// fp32 solve / fused step for K <= 5. Tile path (see run_tile), or bucketed:
+// classify paths by kind mask on the device, then one specialised kernel per
+// non-empty mask — the staged TMA kernel on the mask's row range when it is
+// contiguous, the gathering kernel over a row permutation otherwise — on side
+// streams so tails overlap.
 template <typename R>
 static int dispatch(int K, const PathArgs<R>& a, int op, cudaStream_t s, bool allow_bucketing = true) {
   constexpr bool is_f32 = sizeof(R) == sizeof(float);
   const int64_t B = a.B;
-  const bool bucketed = is_f32 && allow_bucketing && g_policy.load() != FP_POLICY_DENSE && K >= 1 &&
+  const int policy = g_policy.load();
+  const bool bucketed = is_f32 && allow_bucketing && policy != FP_POLICY_DENSE && K >= 1 &&
                         K <= kMaxSpecialisedOrder && (op == OP_SOLVE || op == OP_SOLVE_VJP) &&
                         B > 0 && B < (int64_t(1) << 31) && a.rows == nullptr;
   if (!bucketed) return dispatch_dense_k<R>(K, a, op, s);
   if constexpr (is_f32) {
+    if (K <= kMaxTileOrder &&
+        (policy == FP_POLICY_TILE || (policy == FP_POLICY_AUTO && tile_preferred(K))))
+      return cuda_status(run_tile(K, a, op, s));
     BucketScratch sc;
     BucketPlan plan;
     cudaError_t e = bucket_plan<float>(a.basis, B, K, sc, plan, s);
+    if (e == cudaSuccess) record_mixed_fraction(K, plan.mixed_warps, B);
     if (e == cudaSuccess && !plan.all_contiguous) e = bucket_scatter(B, plan, sc, s);
     int live = 0;
     for (int m = 0; m < plan.nb; ++m) live += plan.count[m] > 0;
@@ -589,7 +668,8 @@ int fp_init_params_f64(const double* basis, const double* anchor, const double* 
 uint64_t fp_launch_count(void) { return g_launches.load(); }
 
 int fp_set_kernel_policy(int policy) {
-  if (policy != FP_POLICY_AUTO && policy != FP_POLICY_DENSE && policy != FP_POLICY_AUTO_SERIAL)
+  if (policy != FP_POLICY_AUTO && policy != FP_POLICY_DENSE && policy != FP_POLICY_AUTO_SERIAL &&
+      policy != FP_POLICY_BUCKET && policy != FP_POLICY_TILE)
     return FP_ERR_INVALID_ARGUMENT;
   g_policy.store(policy);
   return FP_OK;

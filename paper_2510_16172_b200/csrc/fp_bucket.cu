@@ -21,10 +21,12 @@ namespace fp {
 template <typename R>
 __global__ void classify_kernel(const R* __restrict__ basis, int64_t B, int K,
                                 uint8_t* __restrict__ codes, unsigned long long* __restrict__ stats) {
-  // stats: [0, nb) counts, [nb, 2nb) min row, [2nb, 3nb) max row
+  // stats: [0, nb) counts, [nb, 2nb) min row, [2nb, 3nb) max row, [3nb] mixed warps
   __shared__ unsigned int hist[kMaxBuckets];
   __shared__ unsigned long long lo[kMaxBuckets], hi[kMaxBuckets];
+  __shared__ unsigned int mixed;
   const int nb = 1 << K;
+  if (threadIdx.x == 0) mixed = 0;
   for (int i = threadIdx.x; i < nb; i += blockDim.x) {
     hist[i] = 0;
     lo[i] = ~0ull;
@@ -57,9 +59,11 @@ __global__ void classify_kernel(const R* __restrict__ basis, int64_t B, int K,
         atomicMin(&lo[code], first);
         atomicMax(&hi[code], lastrow);
       }
+      if (lane == __ffs(live_mask) - 1 && same != live_mask) atomicAdd(&mixed, 1u);
     }
   }
   __syncthreads();
+  if (threadIdx.x == 0 && mixed) atomicAdd(&stats[3 * nb], (unsigned long long)mixed);
   for (int i = threadIdx.x; i < nb; i += blockDim.x) {
     if (!hist[i]) continue;
     atomicAdd(&stats[i], (unsigned long long)hist[i]);
@@ -75,6 +79,7 @@ __global__ void stats_init_kernel(unsigned long long* stats, int nb) {
     stats[nb + i] = ~0ull;
     stats[2 * nb + i] = 0;
   }
+  if (i == 0) stats[3 * nb] = 0;
 }
 
 __global__ void scatter_kernel(const uint8_t* __restrict__ codes, int64_t B,
@@ -112,21 +117,22 @@ cudaError_t bucket_plan(const R* basis, int64_t B, int K, BucketScratch& sc, Buc
   plan.nb = nb;
   cudaError_t e;
   if ((e = cudaMallocAsync(&sc.codes, size_t(B), s)) != cudaSuccess) return e;
-  if ((e = cudaMallocAsync(&sc.small, sizeof(unsigned long long) * 4 * kMaxBuckets, s)) != cudaSuccess)
+  if ((e = cudaMallocAsync(&sc.small, sizeof(unsigned long long) * (4 * kMaxBuckets + 1), s)) != cudaSuccess)
     return e;
-  static unsigned long long* host = nullptr;  // pinned staging for the 3 x nb stats
+  static unsigned long long* host = nullptr;  // pinned staging for the 3 x nb + 1 stats
   if (host == nullptr) {
-    if ((e = cudaMallocHost(&host, sizeof(unsigned long long) * 3 * kMaxBuckets)) != cudaSuccess)
+    if ((e = cudaMallocHost(&host, sizeof(unsigned long long) * (3 * kMaxBuckets + 1))) != cudaSuccess)
       return e;
   }
   stats_init_kernel<<<1, kMaxBuckets, 0, s>>>(sc.small, nb);
   classify_kernel<R><<<grid_for(B, 256), 256, 0, s>>>(basis, B, K, sc.codes, sc.small);
   count_launches(2);
-  if ((e = cudaMemcpyAsync(host, sc.small, sizeof(unsigned long long) * 3 * nb,
+  if ((e = cudaMemcpyAsync(host, sc.small, sizeof(unsigned long long) * (3 * nb + 1),
                            cudaMemcpyDeviceToHost, s)) != cudaSuccess)
     return e;
   if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
   plan.all_contiguous = true;
+  plan.mixed_warps = int64_t(host[3 * nb]);
   int64_t off = 0;
   for (int m = 0; m < nb; ++m) {
     plan.count[m] = int64_t(host[m]);
@@ -145,7 +151,7 @@ cudaError_t bucket_scatter(int64_t B, const BucketPlan& plan, BucketScratch& sc,
   if ((e = cudaMallocAsync(&sc.rows, size_t(B) * sizeof(int32_t), s)) != cudaSuccess) return e;
   unsigned long long cursor_h[kMaxBuckets];
   for (int m = 0; m < plan.nb; ++m) cursor_h[m] = (unsigned long long)plan.offset[m];
-  unsigned long long* cursor = sc.small + 3 * kMaxBuckets;
+  unsigned long long* cursor = sc.small + 3 * kMaxBuckets + 1;
   if ((e = cudaMemcpyAsync(cursor, cursor_h, sizeof(unsigned long long) * plan.nb,
                            cudaMemcpyHostToDevice, s)) != cudaSuccess)
     return e;

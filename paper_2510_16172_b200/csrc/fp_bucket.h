@@ -13,7 +13,7 @@ constexpr int kMaxBuckets = 1 << kMaxSpecialisedOrder;
 struct BucketScratch {
   uint8_t* codes = nullptr;
   int32_t* rows = nullptr;              // permutation, bucket-major
-  unsigned long long* small = nullptr;  // stats (3 x kMaxBuckets) | cursor
+  unsigned long long* small = nullptr;  // stats (3 x kMaxBuckets + 1) | cursor
 };
 
 struct BucketPlan {
@@ -21,6 +21,7 @@ struct BucketPlan {
   int64_t count[kMaxBuckets], lo[kMaxBuckets], hi[kMaxBuckets], offset[kMaxBuckets];
   bool contiguous[kMaxBuckets];
   bool all_contiguous = true;
+  int64_t mixed_warps = 0;  // warps of 32 consecutive rows with more than one mask
 };
 
 // Classify + per-mask statistics; synchronises `s` to bring the plan home.

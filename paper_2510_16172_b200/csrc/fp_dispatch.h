@@ -20,6 +20,10 @@ cudaError_t dispatch_masked_solve(const PathArgs<float>& a, unsigned mask, cudaS
 template <int K>
 cudaError_t dispatch_masked_solve_vjp(const PathArgs<float>& a, unsigned mask, cudaStream_t s);
 
+// Tile kernels (per-warp kind-mask dispatch, fp32, K <= 5); fp_inst.cu part 3.
+template <int K>
+cudaError_t dispatch_tile(const PathArgs<float>& a, int op, cudaStream_t s);
+
 void count_launches(uint64_t n);
 
 }  // namespace fp

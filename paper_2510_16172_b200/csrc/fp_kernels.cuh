@@ -37,6 +37,8 @@ struct PathArgs {
   // paths (a kind-mask bucket that is not one contiguous range).
   const int32_t* rows;
   int64_t n_rows;
+  // Tile kernels: count of warps whose paths have different kind masks (nullable).
+  unsigned long long* mixed_warps;
 };
 
 // Per-path output destinations (shared-memory slab slots or global records).
@@ -277,6 +279,36 @@ __device__ __forceinline__ void run_path(const PathArgs<R>& a, int64_t row, cons
   if (o.st) o.st[0] = st;
 }
 
+// ---- per-warp kind-mask dispatch (the "tile" kernels) -------------------------
+// MASK == kAnyMask instantiates path_kernel with every specialised variant of
+// order K inlined: each thread derives its path's kind mask from the staged
+// record (bit i set when interaction i has a nonzero second basis column,
+// geometry.py:74-77 — the classify_kernel rule) and runs that variant. Warps
+// whose paths share a mask (ordering-major batches, every warp but the
+// boundaries) run one variant; a mixed warp runs each lane's own variant under
+// SIMT divergence, so a path's bits never depend on its neighbours. No
+// classification pass, no host round trip, one launch.
+constexpr unsigned kAnyMask = 0xFFFFFFFFu;
+
+template <int K>
+__device__ __forceinline__ unsigned rec_mask(const Rec<float, K>& in) {
+  unsigned m = 0;
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+    m |= unsigned(in.b[6 * i + 1] != 0.f || in.b[6 * i + 3] != 0.f || in.b[6 * i + 5] != 0.f) << i;
+  return m;
+}
+
+template <int K, int OP, unsigned M = 0>
+__device__ __forceinline__ void run_any_mask(unsigned m, const PathArgs<float>& a, int64_t row,
+                                             const Rec<float, K>& in, bool has_v, int tid) {
+  if (m == M) {
+    run_path<float, K, M, OP>(a, row, in, has_v, tid, true);
+    return;
+  }
+  if constexpr (M + 1 < (1u << K)) run_any_mask<K, OP, M + 1>(m, a, row, in, has_v, tid);
+}
+
 // Copy `width`-element records of the tile from global to shared memory with
 // asynchronous copies (cp.async, LDGSTS): every element's load is in flight
 // at once instead of one load latency per loop trip. Gathered tiles move each
@@ -368,7 +400,17 @@ __device__ __forceinline__ void process_tile(const PathArgs<R>& a, const int32_t
   __syncthreads();
   if (tid < n) {
     const int64_t row = srow ? int64_t(srow[tid]) : base + tid;
-    run_path<R, K, MASK, OP>(a, row, in, has_v, tid, true);
+    if constexpr (MASK == kAnyMask) {
+      const unsigned m = rec_mask<K>(in);
+      if (a.mixed_warps != nullptr) {
+        const unsigned act = __activemask();
+        if (__match_any_sync(act, m) != act && (tid & 31) == __ffs(act) - 1)
+          atomicAdd(a.mixed_warps, 1ull);
+      }
+      run_any_mask<K, OP>(m, a, row, in, has_v, tid);
+    } else {
+      run_path<R, K, MASK, OP>(a, row, in, has_v, tid, true);
+    }
   }
   fence_async_smem();  // make the slab writes visible to the TMA (async) proxy
   __syncthreads();
