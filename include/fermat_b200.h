@@ -195,6 +195,12 @@ int fp_image_method_f64(const double* basis, const double* anchor, const double*
  * bench times it with CUDA events to measure the FP32 SIMT peak. */
 int fp_peak_ffma(int blocks, int iters, float* out, void* stream);
 
+/* Benchmark utility: enqueue a kernel that holds `stream` until the host
+ * stores a nonzero int at host_flag (pinned host memory) or timeout_s
+ * (<= 60) elapses. bench.py gates its timed region with it so every timed
+ * step is enqueued before the device starts. */
+int fp_gate_wait(const int* host_flag, double timeout_s, void* stream);
+
 /* ---- bookkeeping ---------------------------------------------------------- */
 /* Kernel selection for fp32 solves / fused steps (other calls run the dense
  * kernels). Every policy runs, for each path, the kernel variant carrying only

@@ -102,14 +102,20 @@ static cudaError_t masked_k(int K, const PathArgs<float>& a, int op, unsigned m,
 constexpr int kMaxTileOrder = 3;
 constexpr double kMaxMixedFraction = 0.125;
 
+// Re-probe the layout every kProbeEvery tile calls of an order (the other
+// calls launch the kernel alone).
+constexpr int kProbeEvery = 16;
+
 struct LayoutProbe {
   std::mutex mu;
   bool init[kMaxTileOrder + 1] = {};
   bool pending[kMaxTileOrder + 1] = {};
   cudaEvent_t ev[kMaxTileOrder + 1];
   unsigned long long* host = nullptr;  // pinned, one slot per order
+  unsigned long long* dev = nullptr;   // device counters, one per order
   int64_t warps[kMaxTileOrder + 1] = {};
   double frac[kMaxTileOrder + 1] = {};
+  int since[kMaxTileOrder + 1] = {};   // tile calls since the last probe
 };
 static LayoutProbe& probe() {
   static LayoutProbe p;
@@ -136,34 +142,42 @@ static void record_mixed_fraction(int K, int64_t mixed, int64_t B) {
 
 static cudaError_t run_tile(int K, const PathArgs<float>& a0, int op, cudaStream_t s) {
   PathArgs<float> a = a0;
-  unsigned long long* dev = nullptr;
-  cudaError_t e = cudaMallocAsync(&dev, sizeof(unsigned long long), s);
-  if (e != cudaSuccess) return e;
-  if ((e = cudaMemsetAsync(dev, 0, sizeof(unsigned long long), s)) != cudaSuccess) return e;
-  a.mixed_warps = dev;
+  LayoutProbe& p = probe();
+  cudaError_t e = cudaSuccess;
+  bool probing = false;
+  {
+    std::lock_guard<std::mutex> lk(p.mu);
+    if (!p.init[K]) {
+      if (p.host == nullptr)
+        e = cudaMallocHost(&p.host, sizeof(unsigned long long) * (kMaxTileOrder + 1));
+      if (e == cudaSuccess && p.dev == nullptr)
+        e = cudaMalloc(&p.dev, sizeof(unsigned long long) * (kMaxTileOrder + 1));
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p.ev[K], cudaEventDisableTiming);
+      if (e != cudaSuccess) return e;
+      p.init[K] = true;
+      p.since[K] = kProbeEvery;
+    }
+    probing = !p.pending[K] && ++p.since[K] >= kProbeEvery;
+    if (probing) {
+      p.since[K] = 0;
+      if ((e = cudaMemsetAsync(p.dev + K, 0, sizeof(unsigned long long), s)) != cudaSuccess) return e;
+      a.mixed_warps = p.dev + K;
+    }
+  }
   switch (K) {
     case 1: e = dispatch_tile<1>(a, op, s); break;
     case 2: e = dispatch_tile<2>(a, op, s); break;
     default: e = dispatch_tile<3>(a, op, s); break;
   }
   count_launches(1);
-  if (e == cudaSuccess) {
-    LayoutProbe& p = probe();
+  if (e == cudaSuccess && probing) {
     std::lock_guard<std::mutex> lk(p.mu);
-    if (p.host == nullptr) e = cudaMallocHost(&p.host, sizeof(unsigned long long) * (kMaxTileOrder + 1));
-    if (e == cudaSuccess && !p.init[K]) {
-      e = cudaEventCreateWithFlags(&p.ev[K], cudaEventDisableTiming);
-      p.init[K] = e == cudaSuccess;
-    }
-    if (e == cudaSuccess && !p.pending[K]) {
-      e = cudaMemcpyAsync(p.host + K, dev, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
-      if (e == cudaSuccess) e = cudaEventRecord(p.ev[K], s);
-      p.warps[K] = (a.B - a.row_begin + 31) / 32;
-      p.pending[K] = e == cudaSuccess;
-    }
+    e = cudaMemcpyAsync(p.host + K, p.dev + K, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaEventRecord(p.ev[K], s);
+    p.warps[K] = (a.B - a.row_begin + 31) / 32;
+    p.pending[K] = e == cudaSuccess;
   }
-  cudaError_t f = cudaFreeAsync(dev, s);
-  return e != cudaSuccess ? e : f;
+  return e;
 }
 
 // fp32 solve / fused step for K <= 5. Tile path (see run_tile), or bucketed:

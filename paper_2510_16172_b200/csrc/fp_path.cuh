@@ -69,10 +69,18 @@ __device__ __forceinline__ double2 add2(double2 a, double2 b) { return make_doub
 __device__ __forceinline__ double2 neg2(double2 a) { return make_double2(-a.x, -a.y); }
 __device__ __forceinline__ double2 sub2(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 
-template <typename P>
-__device__ __forceinline__ auto& lane(P& p, int h) { return h ? p.y : p.x; }
+// Lane access by value / by store (never a reference picked by a condition:
+// a selected pointer into the pair defeats scalar replacement and sends the
+// whole state to local memory in the large tile kernels).
 template <typename P>
 __device__ __forceinline__ auto lane(const P& p, int h) { return h ? p.y : p.x; }
+template <typename P, typename V>
+__device__ __forceinline__ void set_lane(P& p, int h, V v) {
+  if (h)
+    p.y = v;
+  else
+    p.x = v;
+}
 
 // Vectors over the NA unknowns: NP pairs, element j in lane j & 1 of pair j >> 1.
 template <int NA>
@@ -81,6 +89,7 @@ struct Packed {
   static constexpr int NF = NA / 2;        // full pairs (no padding lane)
 };
 #define FP_EL(v, j) lane((v)[(j) >> 1], (j) & 1)
+#define FP_SET(v, j, x) set_lane((v)[(j) >> 1], (j) & 1, (x))
 
 // v . w over the NA real elements: lane-wise pair chains, then the two lanes
 // (and the unpaired last element of an odd NA).
@@ -186,8 +195,8 @@ struct PathState {
   R rn[S];        // 1 / max(|s_k|, eps)
   R nu[S];        // |s_k| (unclamped; valid after eval<false> / finish_norms)
 
-  __device__ __forceinline__ R& T(int j) { return FP_EL(t, j); }
   __device__ __forceinline__ R T(int j) const { return FP_EL(t, j); }
+  __device__ __forceinline__ void setT(int j, R v) { FP_SET(t, j, v); }
   __device__ __forceinline__ R Gr(int j) const { return FP_EL(g, j); }
   __device__ __forceinline__ R S3(int k, int r) const {
     return r == 0 ? sxy[k].x : (r == 1 ? sxy[k].y : sz[k]);
@@ -220,18 +229,18 @@ struct PathState {
     Pz[0] = G.x0z;
     Pxy[K + 1] = G.xexy;
     Pz[K + 1] = G.xez;
-#pragma unroll
-    for (int i = 0; i < K; ++i) {
+    static_for<K>([&](auto ic) {
+      constexpr int i = decltype(ic)::value;
       // b_i + A_i0 t_i0 (+ A_i1 t_i1) as one explicit FMA chain
       const R t0 = T(L::idx(i, 0));
       Pxy[i + 1] = fma2(G.Axy[i][0], bc2(t0), G.bxy[i]);
       Pz[i + 1] = fma(G.Az[i][0], t0, G.bz[i]);
-      if (L::plane(i)) {
+      if constexpr (L::plane(i)) {
         const R t1 = T(L::idx(i, 1));
         Pxy[i + 1] = fma2(G.Axy[i][1], bc2(t1), Pxy[i + 1]);
         Pz[i + 1] = fma(G.Az[i][1], t1, Pz[i + 1]);
       }
-    }
+    });
   }
 
   // Points as plain 3-vectors (outputs).
@@ -278,9 +287,9 @@ struct PathState {
     for (int i = 0; i < K; ++i) {
       const V2<R> qxy = sub2(uxy[i], uxy[i + 1]);
       const R qz = uz[i] - uz[i + 1];
-      FP_EL(gout, L::idx(i, 0)) = fma(G.Az[i][0], qz, fma(G.Axy[i][0].y, qxy.y, G.Axy[i][0].x * qxy.x));
+      FP_SET(gout, L::idx(i, 0), fma(G.Az[i][0], qz, fma(G.Axy[i][0].y, qxy.y, G.Axy[i][0].x * qxy.x)));
       if (L::plane(i))
-        FP_EL(gout, L::idx(i, 1)) = fma(G.Az[i][1], qz, fma(G.Axy[i][1].y, qxy.y, G.Axy[i][1].x * qxy.x));
+        FP_SET(gout, L::idx(i, 1), fma(G.Az[i][1], qz, fma(G.Axy[i][1].y, qxy.y, G.Axy[i][1].x * qxy.x)));
     }
   }
 

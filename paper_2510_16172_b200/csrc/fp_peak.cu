@@ -29,7 +29,28 @@ __global__ void __launch_bounds__(256) ffma_peak_kernel(int iters, float seed, f
   if (s == 1234.5f) out[0] = s;  // keep the chains alive
 }
 
+// Benchmark gate: holds the stream until the host sets *flag (pinned host
+// memory, read over the mapping), so a timed region can be enqueued in full
+// before the device starts it; host-side jitter then never idles the GPU
+// inside a timed step. Bounded by timeout_ns (globaltimer) so it cannot hang.
+__global__ void gate_kernel(const volatile int* flag, unsigned long long timeout_ns) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (*flag == 0) {
+    __nanosleep(1000);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > timeout_ns) break;
+  }
+}
+
 }  // namespace fp
+
+extern "C" int fp_gate_wait(const int* host_flag, double timeout_s, void* stream) {
+  if (host_flag == nullptr || !(timeout_s > 0.0) || timeout_s > 60.0) return FP_ERR_INVALID_ARGUMENT;
+  fp::gate_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(
+      host_flag, static_cast<unsigned long long>(timeout_s * 1e9));
+  return cudaGetLastError() == cudaSuccess ? FP_OK : FP_ERR_CUDA;
+}
 
 extern "C" int fp_peak_ffma(int blocks, int iters, float* out, void* stream) {
   if (blocks < 1 || iters < 1) return FP_ERR_INVALID_ARGUMENT;
