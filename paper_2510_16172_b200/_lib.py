@@ -134,6 +134,7 @@ POLICY_DENSE = 1
 POLICY_AUTO_SERIAL = 2
 POLICY_BUCKET = 3
 POLICY_TILE = 4
+TILE_MAX_ORDER = 5  # fp_abi.cu kAutoTileMaxOrder: orders with a host-sync-free dispatch
 
 
 def set_kernel_policy(policy: str) -> None:

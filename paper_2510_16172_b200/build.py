@@ -28,7 +28,7 @@ OBJ_DIR = os.path.join(REPO, "build", "obj")
 
 ORDERS = range(1, 9)
 SPECIALISED_MAX_ORDER = 5  # fp_bucket.h kMaxSpecialisedOrder
-TILE_MAX_ORDER = 3  # fp_abi.cu kMaxTileOrder (every mask inlined in one kernel)
+TILE_MAX_ORDER = 5  # fp_abi.cu kMaxTileOrder (every mask of the order in one kernel)
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo", "-fmad=false", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",

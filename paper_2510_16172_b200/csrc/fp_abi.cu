@@ -99,7 +99,11 @@ static cudaError_t masked_k(int K, const PathArgs<float>& a, int op, unsigned m,
 // event, read by a later call once the event has completed — no sync). The
 // bucketed path learns the same number from its classification. AUTO keeps
 // using the tile kernel while the last known mixed fraction is small.
-constexpr int kMaxTileOrder = 3;
+constexpr int kMaxTileOrder = 5;
+#ifndef FP_AUTO_TILE_MAX_ORDER
+#define FP_AUTO_TILE_MAX_ORDER 5
+#endif
+constexpr int kAutoTileMaxOrder = FP_AUTO_TILE_MAX_ORDER;  // orders AUTO sends to the tile kernel
 constexpr double kMaxMixedFraction = 0.125;
 
 // Re-probe the layout every kProbeEvery tile calls of an order (the other
@@ -167,7 +171,9 @@ static cudaError_t run_tile(int K, const PathArgs<float>& a0, int op, cudaStream
   switch (K) {
     case 1: e = dispatch_tile<1>(a, op, s); break;
     case 2: e = dispatch_tile<2>(a, op, s); break;
-    default: e = dispatch_tile<3>(a, op, s); break;
+    case 3: e = dispatch_tile<3>(a, op, s); break;
+    case 4: e = dispatch_tile<4>(a, op, s); break;
+    default: e = dispatch_tile<5>(a, op, s); break;
   }
   count_launches(1);
   if (e == cudaSuccess && probing) {
@@ -195,8 +201,8 @@ static int dispatch(int K, const PathArgs<R>& a, int op, cudaStream_t s, bool al
                         B > 0 && B < (int64_t(1) << 31) && a.rows == nullptr;
   if (!bucketed) return dispatch_dense_k<R>(K, a, op, s);
   if constexpr (is_f32) {
-    if (K <= kMaxTileOrder &&
-        (policy == FP_POLICY_TILE || (policy == FP_POLICY_AUTO && tile_preferred(K))))
+    if ((K <= kMaxTileOrder && policy == FP_POLICY_TILE) ||
+        (K <= kAutoTileMaxOrder && policy == FP_POLICY_AUTO && tile_preferred(K)))
       return cuda_status(run_tile(K, a, op, s));
     BucketScratch sc;
     BucketPlan plan;

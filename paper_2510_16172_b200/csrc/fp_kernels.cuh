@@ -299,11 +299,24 @@ __device__ __forceinline__ unsigned rec_mask(const Rec<float, K>& in) {
   return m;
 }
 
+// Orders above kInlineTileMaxOrder keep each variant a separate (noinline)
+// function: ptxas compiles 2^K inlined solvers in one function too slowly.
+constexpr int kInlineTileMaxOrder = 3;
+
+template <int K, int OP, unsigned M>
+__device__ __noinline__ void run_variant(const PathArgs<float>& a, int64_t row, const Rec<float, K>& in,
+                                         bool has_v, int tid) {
+  run_path<float, K, M, OP>(a, row, in, has_v, tid, true);
+}
+
 template <int K, int OP, unsigned M = 0>
 __device__ __forceinline__ void run_any_mask(unsigned m, const PathArgs<float>& a, int64_t row,
                                              const Rec<float, K>& in, bool has_v, int tid) {
   if (m == M) {
-    run_path<float, K, M, OP>(a, row, in, has_v, tid, true);
+    if constexpr (K <= kInlineTileMaxOrder)
+      run_path<float, K, M, OP>(a, row, in, has_v, tid, true);
+    else
+      run_variant<K, OP, M>(a, row, in, has_v, tid);
     return;
   }
   if constexpr (M + 1 < (1u << K)) run_any_mask<K, OP, M + 1>(m, a, row, in, has_v, tid);
@@ -492,16 +505,26 @@ struct MinBlocks {
 #ifndef FP_TILE_MIN_BLOCKS_K3
 #define FP_TILE_MIN_BLOCKS_K3 4
 #endif
+#ifndef FP_TILE_MIN_BLOCKS_K4
+#define FP_TILE_MIN_BLOCKS_K4 3
+#endif
+#ifndef FP_TILE_MIN_BLOCKS_K5
+#define FP_TILE_MIN_BLOCKS_K5 2
+#endif
 template <typename R, int K, unsigned MASK>
 struct LaunchMin {
   static constexpr int value =
       MASK != kAnyMask ? MinBlocks<R, Lay<K, MASK>::NA>::value
-                       : (K == 1 ? FP_TILE_MIN_BLOCKS_K1 : (K == 2 ? FP_TILE_MIN_BLOCKS_K2 : FP_TILE_MIN_BLOCKS_K3));
+                       : (K == 1   ? FP_TILE_MIN_BLOCKS_K1
+                          : K == 2 ? FP_TILE_MIN_BLOCKS_K2
+                          : K == 3 ? FP_TILE_MIN_BLOCKS_K3
+                          : K == 4 ? FP_TILE_MIN_BLOCKS_K4
+                                   : FP_TILE_MIN_BLOCKS_K5);
 };
 
 template <typename R, int K, unsigned MASK, int OP>
 __global__ void __launch_bounds__(kThreads, (LaunchMin<R, K, MASK>::value))
-    path_kernel(const PathArgs<R> a) {
+    path_kernel(const __grid_constant__ PathArgs<R> a) {
   __shared__ __align__(8) uint64_t bar;
   __shared__ int32_t srow[kThreads];
   const int tid = threadIdx.x;
