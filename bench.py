@@ -435,7 +435,8 @@ def run_scene(args):
     import torch
 
     from paper_2510_16172_b200 import _lib
-    from paper_2510_16172_b200.scene import DeviceScene, candidate_count, make_urban_scene, trace
+    from paper_2510_16172_b200.scene import (DeviceScene, blockers, candidate_count, make_urban_scene,
+                                             trace, visibility)
 
     ws, rank, local = _dist()
     if ws > 1:
@@ -453,9 +454,15 @@ def run_scene(args):
     total = candidate_count(sc, 3)
     cap = 0 if args.no_records else None
 
+    vis = args.visibility and not args.no_records
+    blk = blockers(sc) if vis else None
+
     def step():
-        return trace(sc, max_order=3, iterations=args.iterations, capacity=cap, with_grad=grad,
-                     device_scene=ds)
+        r = trace(sc, max_order=3, iterations=args.iterations, capacity=cap, with_grad=grad,
+                  device_scene=ds, points=vis)
+        if vis:
+            r.vis = [visibility(sc, o, device_scene=ds, blocker_array=blk)[0] for o in r.orders]
+        return r
 
     for _ in range(args.warmup):
         res = step()
@@ -494,6 +501,24 @@ def run_scene(args):
         if grad:
             line["loss"] = res.loss
             line["grad_norm"] = float(torch.linalg.vector_norm(res.vertex_grad).item())
+        if vis:
+            # visibility stage alone (csrc/fp_visibility.cu), on the last step's records
+            v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            v0.record()
+            for o in res.orders:
+                visibility(sc, o, device_scene=ds, blocker_array=blk)
+            v1.record()
+            torch.cuda.synchronize()
+            for d, o, f in zip(per_order, res.orders, res.vis):
+                d["records"] = int(f.numel())
+                d["visible"] = int((f == 0).sum().item())
+                d["blocked"] = int(((f & _lib.VIS_BLOCKED) != 0).sum().item())
+                d["wrong_side"] = int(((f & _lib.VIS_WRONG_SIDE) != 0).sum().item())
+            nrec = sum(int(f.numel()) for f in res.vis)
+            line["visibility"] = {"blockers": int(blk.shape[0]), "records": nrec,
+                                  "ms": v0.elapsed_time(v1),
+                                  "paths_per_s": nrec / max(v0.elapsed_time(v1) * 1e-3, 1e-12),
+                                  "note": "included in ms_per_step (trace with points + visibility)"}
         print(json.dumps(line), flush=True)
     if ws > 1:
         import torch.distributed as dist
@@ -593,6 +618,8 @@ def main(argv=None):
     ap.add_argument("--alphabet", choices=("all", "walls"), default="all",
                     help="config3/4 objects: walls + edges (192) or the 64 walls only")
     ap.add_argument("--no-records", action="store_true", help="config3: counts only")
+    ap.add_argument("--visibility", action="store_true",
+                    help="config3/4: also flag occluded / wrong-side paths (fp_visibility_f64)")
     args = ap.parse_args(argv)
     if args.workload in ("config3", "config4") and args.impl == "ours":
         return run_scene(args)

@@ -166,6 +166,25 @@ int fp_enum_trace_f32(const float* obj_basis, const float* obj_anchor, const int
 int fp_vertex_chain_f32(const float* obj_grad, int n_objects, const int32_t* vert_ids,
                         const float* coef, float* vertex_grad, void* stream);
 
+/* ---- visibility of traced paths (post-processing; no reference code) --------
+ * For n traced paths of order 1..3 (TX, interaction points (n, order, 3), RX =
+ * rx[rec_rx[r]]), flags[r] gets
+ *   FP_VIS_BLOCKED     a segment crosses one of the n_blockers parallelograms
+ *                      O + a U + b V (blockers (Q, 3, 3) = O, U, V; a, b in
+ *                      [0, 1]) farther than eps metres from both its ends;
+ *   FP_VIS_WRONG_SIDE  (when rec_seq is given) a reflection (obj_plane[o] != 0
+ *                      for object o = rec_seq[r, i], normal = column 0 x
+ *                      column 1 of obj_basis[o]) whose neighbours are not
+ *                      strictly on one side of the plane.
+ * first_blocker[r] (nullable) = index of the first blocker hit, -1 if none.
+ * fp64, unfused, in oracle/visibility_oracle.py's operation order. Q <= 2048. */
+#define FP_VIS_BLOCKED 0x01
+#define FP_VIS_WRONG_SIDE 0x02
+int fp_visibility_f64(const double* blockers, int n_blockers, const float* tx, const float* rx,
+                      const int32_t* rec_rx, const float* points, const int32_t* rec_seq,
+                      const float* obj_basis, const uint8_t* obj_plane, int n_objects, int64_t n,
+                      int order, double eps, uint8_t* flags, int32_t* first_blocker, void* stream);
+
 /* ---- comparison solvers -------------------------------------
  * Damped Newton on active coordinates with step halving: baselines._newton_kernel
  * (baselines.py:152-193), the config-1 comparator. K <= 5. trace_gnorm

@@ -33,6 +33,8 @@ STATUS_DEGENERATE_FINAL = 0x10
 STATUS_SINGULAR = 0x20
 STATUS_OUT_OF_BOUNDS = 0x40
 STATUS_SHORT_SEGMENT = 0x80
+VIS_BLOCKED = 0x01      # fp_visibility_f64 flags
+VIS_WRONG_SIDE = 0x02
 STATUS_UNCONVERGED_MASK = (STATUS_DEGENERATE_ENTRY | STATUS_NOT_STATIONARY
                            | STATUS_NONFINITE | STATUS_DEGENERATE_FINAL)
 
@@ -72,6 +74,7 @@ _SIGS = {
     "fp_enum_trace_f32": [_P, _P, _P, _I, _P, _I, _P, _P, _I, _I, C.c_uint, _I64, _I64, _I, _I,
                           _P, _I64] + [_P] * 9 + [_P],
     "fp_vertex_chain_f32": [_P, _I, _P, _P, _P, _P],
+    "fp_visibility_f64": [_P, _I, _P, _P, _P, _P, _P, _P, _P, _I, _I64, _I, _D, _P, _P, _P],
     "fp_newton_f32": [_P] * 5 + [_I64, _I, _I] + [_P] * 3 + [_P],
     "fp_newton_f64": [_P] * 5 + [_I64, _I, _I] + [_P] * 3 + [_P],
     "fp_image_method_f64": [_P] * 4 + [_I64, _I, _P, _P, _P],

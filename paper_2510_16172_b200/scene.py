@@ -137,6 +137,54 @@ def make_urban_scene(seed: int = 0, n_buildings: int = 16, side: float = 200.0,
     return UrbanScene(np.asarray(walls), tx, rx, alphabet)
 
 
+def blockers(scene: UrbanScene) -> np.ndarray:
+    """Occluders as parallelograms (Q, 3, 3) = (O, U, V), point = O + a U + b V, a, b in [0, 1].
+
+    Every wall quad (O = V0, U = V1 - V0, V = V3 - V0) and, per building (four
+    consecutive walls), its roof spanned by the first two walls' top edges.
+    float64, from the scene's float64 vertices.
+    """
+    V = np.asarray(scene.walls, np.float64)
+    out = [np.stack([V[:, 0], V[:, 1] - V[:, 0], V[:, 3] - V[:, 0]], axis=1)]
+    nb = V.shape[0] // 4
+    if nb:
+        w0, w1 = V[0:4 * nb:4], V[1:4 * nb:4]
+        out.append(np.stack([w0[:, 3], w0[:, 2] - w0[:, 3], w1[:, 2] - w1[:, 3]], axis=1))
+    return np.ascontiguousarray(np.concatenate(out, axis=0))
+
+
+def visibility(scene: UrbanScene, res: "OrderResult", eps: float = 1e-4, wrong_side: bool = True,
+               device_scene: "DeviceScene | None" = None, blocker_array: np.ndarray | None = None):
+    """Visibility flags of traced paths (csrc/fp_visibility.cu): (flags u8, first_blocker i32).
+
+    flags bit 0 (VIS_BLOCKED): a segment crosses a wall or roof farther than
+    `eps` metres from both its ends (the ends lie on the surfaces they interact
+    with, up to the fp32 rounding of the points); bit 1 (VIS_WRONG_SIDE): a reflection whose neighbours are not on one
+    side of the wall. `res` must carry points (trace(..., points=True)).
+    """
+    lib = _lib.load()
+    if res.points is None:
+        raise ValueError("visibility needs interaction points: trace(..., points=True)")
+    ds = device_scene or DeviceScene(scene)
+    dev = ds.basis.device
+    blk = blockers(scene) if blocker_array is None else np.asarray(blocker_array, np.float64)
+    blk_d = torch.from_numpy(np.ascontiguousarray(blk, np.float64)).to(dev)
+    n = int(res.points.shape[0])
+    flags = torch.empty(n, dtype=torch.uint8, device=dev)
+    first = torch.empty(n, dtype=torch.int32, device=dev)
+    if n:
+        plane = torch.from_numpy(scene.obj_plane.astype(np.uint8)).to(dev)
+        pts = res.points.contiguous()
+        rc = lib.fp_visibility_f64(
+            blk_d.data_ptr(), int(blk.shape[0]), ds.tx.data_ptr(), ds.rx.data_ptr(),
+            res.rx.contiguous().data_ptr(), pts.data_ptr(),
+            res.seq.contiguous().data_ptr() if wrong_side else None, ds.basis.data_ptr(),
+            plane.data_ptr(), scene.n_objects, n, res.order, float(eps), flags.data_ptr(),
+            first.data_ptr(), stream_ptr())
+        _lib.check(rc, "fp_visibility_f64")
+    return flags, first
+
+
 def pattern_count(scene: UrbanScene, order: int, pattern: int) -> int:
     """Per-RX number of sequences of a kind pattern (fp_enum_pattern_count)."""
     lib = _lib.load()
