@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <algorithm>
 #include <vector>
 
 #include "fp_bucket.h"
@@ -191,19 +192,26 @@ static cudaError_t run_tile(int K, const PathArgs<float>& a0, int op, cudaStream
 // non-empty mask — the staged TMA kernel on the mask's row range when it is
 // contiguous, the gathering kernel over a row permutation otherwise — on side
 // streams so tails overlap.
+// Routes: any kernel the policy picks; never one that synchronises the
+// stream (tile or dense — for enqueue loops like the host-buffer pipeline);
+// dense only.
+enum Route { kRouteAny = 0, kRouteNoSync = 1, kRouteDense = 2 };
+
 template <typename R>
-static int dispatch(int K, const PathArgs<R>& a, int op, cudaStream_t s, bool allow_bucketing = true) {
+static int dispatch(int K, const PathArgs<R>& a, int op, cudaStream_t s, int route = kRouteAny) {
   constexpr bool is_f32 = sizeof(R) == sizeof(float);
   const int64_t B = a.B;
   const int policy = g_policy.load();
-  const bool bucketed = is_f32 && allow_bucketing && policy != FP_POLICY_DENSE && K >= 1 &&
+  const bool bucketed = is_f32 && route != kRouteDense && policy != FP_POLICY_DENSE && K >= 1 &&
                         K <= kMaxSpecialisedOrder && (op == OP_SOLVE || op == OP_SOLVE_VJP) &&
                         B > 0 && B < (int64_t(1) << 31) && a.rows == nullptr;
   if (!bucketed) return dispatch_dense_k<R>(K, a, op, s);
   if constexpr (is_f32) {
-    if ((K <= kMaxTileOrder && policy == FP_POLICY_TILE) ||
-        (K <= kAutoTileMaxOrder && policy == FP_POLICY_AUTO && tile_preferred(K)))
-      return cuda_status(run_tile(K, a, op, s));
+    const bool tile = (K <= kMaxTileOrder && policy == FP_POLICY_TILE) ||
+                      (K <= kAutoTileMaxOrder && policy == FP_POLICY_AUTO &&
+                       (route == kRouteNoSync || tile_preferred(K)));
+    if (tile) return cuda_status(run_tile(K, a, op, s));
+    if (route == kRouteNoSync) return dispatch_dense_k<R>(K, a, op, s);
     BucketScratch sc;
     BucketPlan plan;
     cudaError_t e = bucket_plan<float>(a.basis, B, K, sc, plan, s);
@@ -299,7 +307,7 @@ static int solve_vjp_impl(const R* basis, const R* anchor, const R* start, const
                           const R* T0, int64_t B, int K, int iterations, int fp_iters, const R* w_L,
                           R w_L_scale, int mode, R* T_out, R* points_out, R* length_out, R* d_basis,
                           R* d_anchor, R* d_start, R* d_end, uint8_t* status_out, cudaStream_t s,
-                          bool allow_bucketing = true) {
+                          int route = kRouteAny) {
   if (B < 0 || iterations < 1 || fp_iters < 1) return FP_ERR_INVALID_ARGUMENT;
   if (mode != FP_VJP_FULL && mode != FP_VJP_ENVELOPE) return FP_ERR_UNSUPPORTED_MODE;
   if (K < 0 || K > FP_MAX_ORDER) return FP_ERR_UNSUPPORTED_ORDER;
@@ -314,7 +322,7 @@ static int solve_vjp_impl(const R* basis, const R* anchor, const R* start, const
   a.d_basis = d_basis; a.d_anchor = d_anchor; a.d_start = d_start; a.d_end = d_end;
   a.status_out = status_out;
   finish_args(a);
-  return dispatch<R>(K, a, OP_SOLVE_VJP, s, allow_bucketing);
+  return dispatch<R>(K, a, OP_SOLVE_VJP, s, route);
 }
 
 // ---- generic-order helpers (scalar API; any K <= 64) ------------------------
@@ -595,9 +603,29 @@ int fp_solve_vjp_host_f32(const float* basis, const float* anchor, const float* 
   }
   const float* hin[5] = {basis, anchor, start, end, T0};
   float* hout[7] = {T_out, points_out, length_out, d_basis, d_anchor, d_start, d_end};
-  int64_t c = 0;
-  for (int64_t lo = 0; lo < B; lo += chunk, ++c) {
-    const int64_t n = (B - lo < chunk) ? (B - lo) : chunk;
+  // Chunk schedule: ramp up from chunk/8 (the device-to-host stream, the
+  // bottleneck, starts after one small copy-in + solve instead of a full one)
+  // and back down at the end (short drain); full chunks in between.
+  std::vector<int64_t> sizes;
+  {
+    const int64_t r[3] = {chunk / 8, chunk / 4, chunk / 2};
+    std::vector<int64_t> head, tail;
+    int64_t left = B;
+    for (int i = 0; i < 3 && left > 0; ++i) {
+      const int64_t h = std::min<int64_t>((r[i] + kThreads - 1) / kThreads * kThreads, left);
+      head.push_back(h);
+      left -= h;
+      if (left <= 0) break;
+      const int64_t t = std::min<int64_t>((r[i] + kThreads - 1) / kThreads * kThreads, left);
+      tail.push_back(t);
+      left -= t;
+    }
+    sizes = head;
+    for (; left > 0; left -= std::min(left, chunk)) sizes.push_back(std::min(left, chunk));
+    sizes.insert(sizes.end(), tail.rbegin(), tail.rend());
+  }
+  int64_t c = 0, lo = 0;
+  for (const int64_t n : sizes) {
     const int si = int(c % nstreams);
     cudaStream_t s = g_pipe.streams[si];
     char* p = static_cast<char*>(g_pipe.bufs[si]);
@@ -618,14 +646,14 @@ int fp_solve_vjp_host_f32(const float* basis, const float* anchor, const float* 
                           cudaMemcpyHostToDevice, s);
       if (e != cudaSuccess) return cuda_status(e);
     }
-    // Dense kernel here: the kind-mask plan synchronises its stream, which
-    // would stall this enqueue loop; the pipeline is PCIe-bound anyway.
+    // Tile kernel (no host round trip): the bucketed plan would synchronise
+    // its stream and stall this enqueue loop.
     int rc = solve_vjp_impl<float>(din[0], din[1], din[2], din[3], din[4], n, K, iterations, fp_iters,
                                    nullptr, w_L_scale, mode, hout[0] ? dout[0] : nullptr,
                                    hout[1] ? dout[1] : nullptr, hout[2] ? dout[2] : nullptr,
                                    hout[3] ? dout[3] : nullptr, hout[4] ? dout[4] : nullptr,
                                    hout[5] ? dout[5] : nullptr, hout[6] ? dout[6] : nullptr,
-                                   status_out ? dst : nullptr, s, /*allow_bucketing=*/false);
+                                   status_out ? dst : nullptr, s, kRouteNoSync);
     if (rc != FP_OK) return rc;
     for (int i = 0; i < 7; ++i) {
       if (w_out[i] == 0 || hout[i] == nullptr) continue;
@@ -637,6 +665,8 @@ int fp_solve_vjp_host_f32(const float* basis, const float* anchor, const float* 
       e = cudaMemcpyAsync(status_out + lo, dst, size_t(n), cudaMemcpyDeviceToHost, s);
       if (e != cudaSuccess) return cuda_status(e);
     }
+    lo += n;
+    ++c;
   }
   for (int i = 0; i < nstreams; ++i) {
     e = cudaStreamSynchronize(g_pipe.streams[i]);

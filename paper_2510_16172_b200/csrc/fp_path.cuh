@@ -532,6 +532,10 @@ __device__ __forceinline__ uint8_t bfgs_solve(const Geo<R, K>& G, PathState<R, K
   V2<R> p[NP];
 #pragma unroll
   for (int m = 0; m < NP; ++m) p[m] = neg2(P.g[m]);  // H = I
+#ifdef FP_UNROLL_ITER
+  constexpr int kUnrollIter = FP_UNROLL_ITER;
+#pragma unroll kUnrollIter
+#endif
   for (int it = 0; it < iterations; ++it) {
     bool zero;
     const R alpha = P.step_size(G, p, fp_iters, zero);
@@ -547,18 +551,14 @@ __device__ __forceinline__ uint8_t bfgs_solve(const Geo<R, K>& G, PathState<R, K
     V2<R> y[NP];
 #pragma unroll
     for (int m = 0; m < NP; ++m) y[m] = sub2(gn[m], P.g[m]);
-    // Curvature test sy > 1e-12 |s| |y| (solver.py:184). |s| |y| <= NA
-    // max|s_j| max|y_j|, so a sy above that bound (the common case) passes
-    // without the two norms; sy <= 0 (or NaN) fails; only the band between
-    // evaluates the reference's test with the norms.
+    // Curvature test sy > 1e-12 |s| |y| (solver.py:184), branch-free: with
+    // paired dot products the two norms cost less than the register moves a
+    // rarely-taken branch forces on the hot path.
     const R sy = dotv<R, NA>(sg, y, G.nz);
-    const R ms = absmaxv<R, NA>(sg), my = absmaxv<R, NA>(y);
-    bool ok = sy > (R(1e-12 * NA * 1.0009765625) * ms) * my;
-    if (!ok && sy > R(0)) {
-      const R ss = dotv<R, NA>(sg, sg, G.nz);
-      const R yy = dotv<R, NA>(y, y, G.nz);
-      ok = sy > (R(1e-12) * sqrt_test(ss)) * sqrt_test(yy);
-    }
+    const R ss = dotv<R, NA>(sg, sg, G.nz);
+    const R yy = dotv<R, NA>(y, y, G.nz);
+    const bool ok = sy > (R(1e-12) * sqrt_test(ss)) * sqrt_test(yy);
+    const R ms = absmaxv<R, NA>(sg);
     H.step(sg, y, gn, p, ok, sy, ms, G.nz);
 #pragma unroll
     for (int m = 0; m < NP; ++m) P.g[m] = gn[m];
