@@ -250,3 +250,35 @@ def test_specialised_kernels_match_dense(K):
     # unconverged paths: most still land on the same answer
     agree = points_ok(spec.points.cpu().numpy(), dense.points.double().cpu().numpy())
     assert agree.mean() > 0.8
+
+
+@pytest.mark.parametrize("K", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("layout", ["ordered", "interleaved"])
+def test_tile_and_bucketed_dispatch_bitwise_equal(K, layout):
+    """Every non-dense policy runs each path through its own kind-mask variant:
+    the tile kernel (per-warp dispatch, mixed warps diverge) and the bucketed
+    per-mask kernels give the same bits, for ordering-major and scattered
+    layouts (include/fermat_b200.h, FP_POLICY_*)."""
+    from paper_2510_16172_b200.solver import solve_with_gradients
+
+    b = datagen.gen_batch(40 + K, datagen.all_orderings(K), 300)
+    if layout == "interleaved":
+        b = datagen.interleave(b, seed=K)
+    sc = BatchScene(b.basis, b.anchor, b.start, b.end)
+    opts = SolveOptions(iterations=20, precision=Precision.SINGLE)
+    out = {}
+    try:
+        for pol in ("tile", "bucket", "serial", "auto"):
+            _lib.set_kernel_policy(pol)
+            res, grads = solve_with_gradients(sc, b.T0, opts)
+            fwd = solve(sc, b.T0, opts)
+            out[pol] = (res, grads, fwd)
+    finally:
+        _lib.set_kernel_policy("auto")
+    ref_res, ref_g, ref_f = out["bucket"]
+    for pol, (res, grads, fwd) in out.items():
+        for x, y in ((res.T, ref_res.T), (res.points, ref_res.points), (res.length, ref_res.length),
+                     (res.status, ref_res.status), (grads.basis, ref_g.basis), (grads.anchor, ref_g.anchor),
+                     (grads.start, ref_g.start), (grads.end, ref_g.end), (fwd.T, ref_f.T),
+                     (fwd.g, ref_f.g), (fwd.points, ref_f.points), (fwd.status, ref_f.status)):
+            assert torch.equal(x, y), pol
