@@ -513,25 +513,19 @@ __device__ __forceinline__ bool stationary(const V2<R> (&g)[Packed<NA>::NP], R l
   return Num<R>::sqrt_(norm2_seq<R, NA>(g)) < R(1e-5) * (R(1) + len);
 }
 
-// The fixed-iteration BFGS loop (solver.py:146-215) from the state P (which
-// must hold t and its evaluation). Returns DEGENERATE_ENTRY / ZERO_DIRECTION
-// status bits; optional per-iteration trace (solver.py:202-206) and final
-// inverse Hessian (return_state) in the dense 2K layout.
-template <typename R, int K, unsigned MASK>
-__device__ __forceinline__ uint8_t bfgs_solve(const Geo<R, K>& G, PathState<R, K, MASK>& P,
-                                              int iterations, int fp_iters, R* trace_len,
-                                              R* trace_gnorm, int64_t trace_ld, int64_t row,
-                                              R* H_out) {
+// The BFGS iterations (solver.py:171-211). GENERAL = false is the common case
+// compiled without the per-iteration checks: one fixed-point step (F = 1, the
+// reference default solver.py:45) and no trace.
+template <typename R, int K, unsigned MASK, bool GENERAL>
+__device__ __forceinline__ void bfgs_iterations(const Geo<R, K>& G, PathState<R, K, MASK>& P,
+                                                InvHess<R, K, MASK>& H,
+                                                V2<R> (&p)[Packed<Lay<K, MASK>::NA>::NP], uint8_t& st,
+                                                int iterations, int fp_iters_rt, R* trace_len,
+                                                R* trace_gnorm, int64_t trace_ld, int64_t row) {
   using L = Lay<K, MASK>;
   constexpr int NA = L::NA;
   constexpr int NP = Packed<NA>::NP;
-  uint8_t st = 0;
-  if (P.min_norm() <= G.eps) st |= FP_STATUS_DEGENERATE_ENTRY;  // checked_segments (solver.py:166)
-  InvHess<R, K, MASK> H;
-  H.identity();
-  V2<R> p[NP];
-#pragma unroll
-  for (int m = 0; m < NP; ++m) p[m] = neg2(P.g[m]);  // H = I
+  const int fp_iters = GENERAL ? fp_iters_rt : 1;
 #ifdef FP_UNROLL_ITER
   constexpr int kUnrollIter = FP_UNROLL_ITER;
 #pragma unroll kUnrollIter
@@ -562,12 +556,40 @@ __device__ __forceinline__ uint8_t bfgs_solve(const Geo<R, K>& G, PathState<R, K
     H.step(sg, y, gn, p, ok, sy, ms, G.nz);
 #pragma unroll
     for (int m = 0; m < NP; ++m) P.g[m] = gn[m];
-    if (trace_len != nullptr) {
+    if (GENERAL && trace_len != nullptr) {
       P.finish_norms(G);
       trace_len[int64_t(it) * trace_ld + row] = P.length();
       trace_gnorm[int64_t(it) * trace_ld + row] = Num<R>::sqrt_(norm2_seq<R, NA>(P.g));
     }
   }
+}
+
+// The fixed-iteration BFGS loop (solver.py:146-215) from the state P (which
+// must hold t and its evaluation). Returns DEGENERATE_ENTRY / ZERO_DIRECTION
+// status bits; optional per-iteration trace (solver.py:202-206) and final
+// inverse Hessian (return_state) in the dense 2K layout.
+template <typename R, int K, unsigned MASK>
+__device__ __forceinline__ uint8_t bfgs_solve(const Geo<R, K>& G, PathState<R, K, MASK>& P,
+                                              int iterations, int fp_iters, R* trace_len,
+                                              R* trace_gnorm, int64_t trace_ld, int64_t row,
+                                              R* H_out) {
+  using L = Lay<K, MASK>;
+  constexpr int NA = L::NA;
+  constexpr int NP = Packed<NA>::NP;
+  uint8_t st = 0;
+  if (P.min_norm() <= G.eps) st |= FP_STATUS_DEGENERATE_ENTRY;  // checked_segments (solver.py:166)
+  InvHess<R, K, MASK> H;
+  H.identity();
+  V2<R> p[NP];
+#pragma unroll
+  for (int m = 0; m < NP; ++m) p[m] = neg2(P.g[m]);  // H = I
+#ifndef FP_NO_LOOP_SPECIALISATION
+  if (fp_iters == 1 && trace_len == nullptr)
+    bfgs_iterations<R, K, MASK, false>(G, P, H, p, st, iterations, 1, nullptr, nullptr, 0, 0);
+  else
+#endif
+    bfgs_iterations<R, K, MASK, true>(G, P, H, p, st, iterations, fp_iters, trace_len, trace_gnorm,
+                                      trace_ld, row);
   P.finish_norms(G);
   if (H_out != nullptr) {
     R* Ho = H_out + row * (4 * K * K);
