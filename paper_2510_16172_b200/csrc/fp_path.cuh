@@ -192,12 +192,14 @@ struct PathState {
   V2<R> g[NP];    // clamped-norm gradient at t
   V2<R> sxy[S];   // segments at t (x, y)
   R sz[S];        //                (z)
-  R rn[S];        // 1 / max(|s_k|, eps)
+  static constexpr int SP = (S + 1) / 2;
+  V2<R> rnp[SP];  // 1 / max(|s_k|, eps), segment pairs (k in lane k & 1 of pair k >> 1)
   R nu[S];        // |s_k| (unclamped; valid after eval<false> / finish_norms)
 
   __device__ __forceinline__ R T(int j) const { return FP_EL(t, j); }
   __device__ __forceinline__ void setT(int j, R v) { FP_SET(t, j, v); }
   __device__ __forceinline__ R Gr(int j) const { return FP_EL(g, j); }
+  __device__ __forceinline__ R RN(int k) const { return FP_EL(rnp, k); }
   __device__ __forceinline__ R S3(int k, int r) const {
     return r == 0 ? sxy[k].x : (r == 1 ? sxy[k].y : sz[k]);
   }
@@ -266,21 +268,37 @@ struct PathState {
     points(G, Pxy, Pz);
     V2<R> uxy[S];
     R uz[S];
+    V2<R> qp[SP];  // squared norms, segment pairs
 #pragma unroll
     for (int k = 0; k < S; ++k) {
       sxy[k] = sub2(Pxy[k + 1], Pxy[k]);
       sz[k] = Pz[k + 1] - Pz[k];
       R q = sxy[k].x * sxy[k].x;
       q = fma(sxy[k].y, sxy[k].y, q);
-      q = fma(sz[k], sz[k], q);
-      if (LIGHT) {
-        rcp_norm(q, G.eps, G.reps, rn[k]);
-      } else {
-        R nc;
-        norm_rcp(q, G.eps, G.reps, nu[k], nc, rn[k]);
+      FP_SET(qp, k, fma(sz[k], sz[k], q));
+    }
+    if (LIGHT) {
+      // reciprocal clamped norms of two segments per paired refinement
+#pragma unroll
+      for (int m = 0; m < S / 2; ++m) rcp_norm2(qp[m], G.eps, G.reps, rnp[m]);
+      if constexpr (S & 1) {
+        R r;
+        rcp_norm(qp[SP - 1].x, G.eps, G.reps, r);
+        rnp[SP - 1] = mk2(r, R(0));
       }
-      uxy[k] = mulz(sxy[k], bc2(rn[k]), G.nz);
-      uz[k] = sz[k] * rn[k];
+    } else {
+#pragma unroll
+      for (int k = 0; k < S; ++k) {
+        R nc, r;
+        norm_rcp(FP_EL(qp, k), G.eps, G.reps, nu[k], nc, r);
+        FP_SET(rnp, k, r);
+      }
+      if constexpr (S & 1) rnp[SP - 1].y = R(0);
+    }
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      uxy[k] = mulz(sxy[k], bc2(RN(k)), G.nz);
+      uz[k] = sz[k] * RN(k);
     }
     if constexpr (NA & 1) gout[NP - 1].y = R(0);
 #pragma unroll
@@ -331,23 +349,23 @@ struct PathState {
       dxy[k] = sub2(wxy[k], wxy[k - 1]);
       dz[k] = wz[k] - wz[k - 1];
     }
-    R a2[S], c[S];
+    V2<R> ca[S];  // {c_k, a2_k}
     R total;
 #pragma unroll
     for (int k = 0; k < S; ++k) {
-      a2[k] = fma(dz[k], dz[k], fma(dxy[k].y, dxy[k].y, dxy[k].x * dxy[k].x));
-      c[k] = fma(dz[k], sz[k], fma(dxy[k].y, sxy[k].y, dxy[k].x * sxy[k].x));
-      total = k == 0 ? a2[0] : total + a2[k];
+      const R a2 = fma(dz[k], dz[k], fma(dxy[k].y, dxy[k].y, dxy[k].x * dxy[k].x));
+      const R cc = fma(dz[k], sz[k], fma(dxy[k].y, sxy[k].y, dxy[k].x * sxy[k].x));
+      ca[k] = mk2(cc, a2);
+      total = k == 0 ? a2 : total + a2;
     }
     zero = total <= Num<R>::tiny();
     R alpha = R(0);
     {
-      R num = c[0] * rn[0], den = a2[0] * rn[0];
+      // {num, den} = sum_k {c_k, a2_k} / max(|s_k|, eps), one paired chain
+      V2<R> nd = mul2(ca[0], bc2(RN(0)));
 #pragma unroll
-      for (int k = 1; k < S; ++k) {
-        num = fma(c[k], rn[k], num);
-        den = fma(a2[k], rn[k], den);
-      }
+      for (int k = 1; k < S; ++k) nd = fma2(ca[k], bc2(RN(k)), nd);
+      const R num = nd.x, den = nd.y;
       const R cand = -div_fast(num, zero ? R(1) : den);
       alpha = (zero || !finite(cand)) ? alpha : cand;
     }
@@ -359,8 +377,8 @@ struct PathState {
         const R e2 = fma(alpha, dz[k], sz[k]);
         R n0, n, ri;
         norm_rcp(fma(e2, e2, fma(exy.y, exy.y, exy.x * exy.x)), G.eps, G.reps, n0, n, ri);
-        num = k == 0 ? c[0] * ri : fma(c[k], ri, num);
-        den = k == 0 ? a2[0] * ri : fma(a2[k], ri, den);
+        num = k == 0 ? ca[0].x * ri : fma(ca[k].x, ri, num);
+        den = k == 0 ? ca[0].y * ri : fma(ca[k].y, ri, den);
       }
       const R cand = -div_fast(num, zero ? R(1) : den);
       alpha = (zero || !finite(cand)) ? alpha : cand;
@@ -658,7 +676,7 @@ __device__ __forceinline__ uint8_t implicit_vjp(const Geo<R, K>& G, const PathSt
 #pragma unroll
   for (int k = 0; k < S; ++k)
 #pragma unroll
-    for (int r = 0; r < 3; ++r) u[k][r] = P.S3(k, r) * P.rn[k];
+    for (int r = 0; r < 3; ++r) u[k][r] = P.S3(k, r) * P.RN(k);
   R q[K][3];
 #pragma unroll
   for (int i = 0; i < K; ++i)
@@ -695,7 +713,7 @@ __device__ __forceinline__ uint8_t implicit_vjp(const Geo<R, K>& G, const PathSt
       gii[0] = fma(G.A(i, 2, 0), G.A(i, 2, 0), fma(G.A(i, 1, 0), G.A(i, 1, 0), G.A(i, 0, 0) * G.A(i, 0, 0)));
       gii[1] = fma(G.A(i, 2, 0), G.A(i, 2, 1), fma(G.A(i, 1, 0), G.A(i, 1, 1), G.A(i, 0, 0) * G.A(i, 0, 1)));
       gii[2] = fma(G.A(i, 2, 1), G.A(i, 2, 1), fma(G.A(i, 1, 1), G.A(i, 1, 1), G.A(i, 0, 1) * G.A(i, 0, 1)));
-      const R ri = P.rn[i], ro = P.rn[i + 1];
+      const R ri = P.RN(i), ro = P.RN(i + 1);
       D[i][0] = (gii[0] - au_in[i][0] * au_in[i][0]) * ri + (gii[0] - au_out[i][0] * au_out[i][0]) * ro;
       D[i][1] = (gii[1] - au_in[i][0] * au_in[i][1]) * ri + (gii[1] - au_out[i][0] * au_out[i][1]) * ro;
       D[i][2] = (gii[2] - au_in[i][1] * au_in[i][1]) * ri + (gii[2] - au_out[i][1] * au_out[i][1]) * ro;
@@ -805,7 +823,7 @@ __device__ __forceinline__ uint8_t implicit_vjp(const Geo<R, K>& G, const PathSt
     }
     const R ud = fma(u[k][2], ds[2], fma(u[k][1], ds[1], u[k][0] * ds[0]));
 #pragma unroll
-    for (int r = 0; r < 3; ++r) w[k][r] = (ds[r] - u[k][r] * ud) * P.rn[k];
+    for (int r = 0; r < 3; ++r) w[k][r] = (ds[r] - u[k][r] * ud) * P.RN(k);
   }
 #pragma unroll
   for (int i = 0; i < K; ++i) {
