@@ -19,7 +19,7 @@ import torch
 
 from . import _lib
 from .batching import BatchScene, device, params_tensor, ptr, stack_params, stream_ptr, to_device
-from .errors import DegenerateSegment, ZeroDirection
+from .errors import DegenerateSegment, ShapeMismatch, ZeroDirection
 from .geometry import PathSpec, check_params
 
 
@@ -158,6 +158,52 @@ def solve_with_gradients(scene: BatchScene, T0=None, opts: SolveOptions = SolveO
                               ptr(grads.end), ptr(res.status), stream_ptr())
     _lib.check(rc, "fp_solve_vjp_f32")
     return res, grads
+
+
+def solve_with_gradients_host(basis, anchor, start, end, T0=None, iterations: int = 20,
+                              fixed_point_iters: int = 1, weight: float = 1.0, mode: str = "full",
+                              chunk: int = 1 << 19, streams: int = 3, out=None):
+    """solve_with_gradients for host (numpy) arrays in the reference layout, fp32.
+
+    One call of fp_solve_vjp_host_f32: the batch streams through the GPU in
+    chunks (copy in, fused solve + VJP, copy out on rotating streams), so host
+    transfers overlap compute. Pinned (page-locked) arrays transfer fastest:
+    pass `out` from `host_buffers` to reuse pinned outputs. Returns a dict of
+    numpy arrays: T, points, length, status, d_basis, d_anchor, d_start, d_end.
+    """
+    lib = _lib.load()
+    f32 = np.float32
+    basis = np.ascontiguousarray(basis, f32)
+    B, K = basis.shape[0], basis.shape[1]
+    anchor = np.ascontiguousarray(anchor, f32)
+    start = np.ascontiguousarray(start, f32)
+    end = np.ascontiguousarray(end, f32)
+    T0 = np.zeros((B, K, 2), f32) if T0 is None else np.ascontiguousarray(T0, f32)
+    if anchor.shape != (B, K, 3) or start.shape != (B, 3) or end.shape != (B, 3) or T0.shape != (B, K, 2):
+        raise ShapeMismatch("host arrays must be basis (B,K,3,2), anchor (B,K,3), start/end (B,3), T0 (B,K,2)")
+    if iterations < 1 or fixed_point_iters < 1:
+        raise ValueError("iterations and fixed_point_iters must be >= 1")
+    out = out if out is not None else host_buffers(B, K, pinned=False)
+    P = lambda a: a.ctypes.data  # noqa: E731
+    rc = lib.fp_solve_vjp_host_f32(P(basis), P(anchor), P(start), P(end), P(T0), B, K, iterations,
+                                   fixed_point_iters, float(weight), _MODES[mode], P(out["T"]),
+                                   P(out["points"]), P(out["length"]), P(out["d_basis"]),
+                                   P(out["d_anchor"]), P(out["d_start"]), P(out["d_end"]),
+                                   P(out["status"]), int(chunk), int(streams))
+    _lib.check(rc, "fp_solve_vjp_host_f32")
+    return out
+
+
+def host_buffers(B: int, K: int, pinned: bool = True) -> dict:
+    """Output arrays for solve_with_gradients_host (page-locked when pinned)."""
+    def mk(shape, dt):
+        if pinned:
+            return torch.empty(shape, dtype=dt, pin_memory=True).numpy()
+        return np.empty(shape, dtype=torch.empty(0, dtype=dt).numpy().dtype)
+    f, u8 = torch.float32, torch.uint8
+    return {"T": mk((B, K, 2), f), "points": mk((B, K, 3), f), "length": mk((B,), f),
+            "status": mk((B,), u8), "d_basis": mk((B, K, 3, 2), f), "d_anchor": mk((B, K, 3), f),
+            "d_start": mk((B, 3), f), "d_end": mk((B, 3), f)}
 
 
 def init_params_batch(scene: BatchScene) -> torch.Tensor:

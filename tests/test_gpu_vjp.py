@@ -138,3 +138,22 @@ def test_fused_step_equals_solve_then_vjp_bitwise():
     _, gw = solve_with_gradients(sc, b.T0, opts, weight=w, mode="full")
     g3, _, _ = vjp_batch(sc, sep.T, w_L=w, mode="full")
     assert torch.equal(gw.anchor, g3.anchor)
+
+
+@pytest.mark.parametrize("K,chunk", [(3, 1024), (5, 512), (6, 256), (1, 1 << 19)])
+def test_host_pipeline_equals_device_step(K, chunk):
+    """fp_solve_vjp_host_f32 (chunked host-buffer pipeline, ramped chunk sizes,
+    pinned and pageable buffers) returns the device-buffer fused step's bits."""
+    from paper_2510_16172_b200.solver import host_buffers, solve_with_gradients_host
+
+    orders = datagen.all_orderings(K) if K <= 3 else datagen.all_orderings(K)[: 6]
+    b = datagen.gen_batch(60 + K, orders, 1700 // len(orders) + 3)  # ragged vs the chunk
+    sc = BatchScene(b.basis, b.anchor, b.start, b.end)
+    res, grads = solve_with_gradients(sc, b.T0, SolveOptions(iterations=20, precision=Precision.SINGLE))
+    for pinned in (True, False):
+        out = solve_with_gradients_host(b.basis, b.anchor, b.start, b.end, b.T0, iterations=20,
+                                        chunk=chunk, out=host_buffers(b.size, K, pinned=pinned))
+        for name, dev in (("T", res.T), ("points", res.points), ("length", res.length),
+                          ("status", res.status), ("d_basis", grads.basis), ("d_anchor", grads.anchor),
+                          ("d_start", grads.start), ("d_end", grads.end)):
+            assert np.array_equal(out[name], dev.cpu().numpy()), (name, pinned)
