@@ -464,6 +464,7 @@ def run_scene(args):
             r.vis = [visibility(sc, o, device_scene=ds, blocker_array=blk)[0] for o in r.orders]
         return r
 
+    peak = measure_ffma_peak(_lib.load(), torch.cuda.current_stream().cuda_stream, dev) if rank == 0 else None
     for _ in range(args.warmup):
         res = step()
     torch.cuda.synchronize()
@@ -498,6 +499,17 @@ def run_scene(args):
             "orders": per_order, "valid_paths": res.valid, "gpu_launches": launches,
             "clocks": sampler.summary(),
         }
+        # FP32 roofline of the whole step by the SURVEY §8(d) convention: every
+        # candidate of order K costs the dense forward count at I iterations
+        # (config 4 adds the VJP count for each valid path); this rank's share.
+        flop = sum(o.candidates * flops_per_path(o.order, args.iterations)[0] for o in res.orders) / ws
+        if grad:
+            flop += sum(o.valid * flops_per_path(o.order, args.iterations)[1] for o in res.orders) / ws
+        achieved = flop / (ms * 1e-3) / 1e12
+        line["roofline"] = {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                            "frac": achieved / peak if peak else None, "traffic": None,
+                            "flop_per_step": flop,
+                            "peak_source": "FFMA microbenchmark (fp_peak_ffma) measured in this run"}
         if grad:
             line["loss"] = res.loss
             line["grad_norm"] = float(torch.linalg.vector_norm(res.vertex_grad).item())
