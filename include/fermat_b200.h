@@ -40,7 +40,7 @@ enum fp_error {
 
 /* Largest interaction count served by the register-resident kernels. The
  * reference allows up to 64 (geometry.py:23); orders above this are rejected. */
-#define FP_MAX_ORDER 8
+#define FP_MAX_ORDER 64 /* geometry.py:23 MAX_INTERACTIONS; orders 9..64 run the warp-per-path solver */
 
 /* ---- per-path status bits (uint8) --------------------------------------- */
 #define FP_STATUS_DEGENERATE_ENTRY 0x01u /* entry segment <= eps: reference raises DegenerateSegment for the batch (solver.py:166) */

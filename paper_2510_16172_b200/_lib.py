@@ -23,7 +23,7 @@ FP_ERR_INVALID_ARGUMENT = 1
 FP_ERR_UNSUPPORTED_ORDER = 2
 FP_ERR_CUDA = 3
 FP_ERR_UNSUPPORTED_MODE = 4
-FP_MAX_ORDER = 8
+FP_MAX_ORDER = 64  # orders 9..64: warp-per-path solver (csrc/fp_wide.cu)
 
 STATUS_DEGENERATE_ENTRY = 0x01
 STATUS_ZERO_DIRECTION = 0x02

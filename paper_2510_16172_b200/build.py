@@ -66,7 +66,8 @@ def _units(orders=ORDERS, obj_dir=None):
         for part in parts:
             units.append((inst, os.path.join(obj_dir, f"fp_inst_k{k}_p{part}.o"),
                           [f"-DFP_INST_K={k}", f"-DFP_INST_PART={part}"]))
-    for extra in ("fp_enum.cu", "fp_bucket.cu", "fp_peak.cu", "fp_baselines.cu", "fp_visibility.cu"):
+    for extra in ("fp_enum.cu", "fp_bucket.cu", "fp_peak.cu", "fp_baselines.cu", "fp_visibility.cu",
+                  "fp_wide.cu"):
         path = os.path.join(CSRC, extra)
         if os.path.exists(path):
             units.append((path, os.path.join(obj_dir, extra.replace(".cu", ".o")), []))

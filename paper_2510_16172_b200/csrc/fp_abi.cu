@@ -76,7 +76,10 @@ static int dispatch_dense_k(int K, const PathArgs<R>& a, int op, cudaStream_t s)
     case 6: e = dispatch_dense<R, 6>(a, op, s); break;
     case 7: e = dispatch_dense<R, 7>(a, op, s); break;
     case 8: e = dispatch_dense<R, 8>(a, op, s); break;
-    default: return FP_ERR_UNSUPPORTED_ORDER;
+    default:
+      if (K > FP_MAX_ORDER) return FP_ERR_UNSUPPORTED_ORDER;
+      e = dispatch_wide<R>(K, a, op, s);
+      break;
   }
   if (a.B > 0) count_launches(1);
   return cuda_status(e);

@@ -24,6 +24,10 @@ cudaError_t dispatch_masked_solve_vjp(const PathArgs<float>& a, unsigned mask, c
 template <int K>
 cudaError_t dispatch_tile(const PathArgs<float>& a, int op, cudaStream_t s);
 
+// Warp-per-path solver for orders 9..64 (fp_wide.cu), every op, fp32/fp64.
+template <typename R>
+cudaError_t dispatch_wide(int K, const PathArgs<R>& a, int op, cudaStream_t s);
+
 void count_launches(uint64_t n);
 
 }  // namespace fp

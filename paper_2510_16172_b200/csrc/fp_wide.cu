@@ -1,0 +1,561 @@
+// Warp-cooperative solver for orders 9..64.
+//
+// The reference accepts up to 64 interactions per path (geometry.py:23,
+// MAX_INTERACTIONS); the register-resident kernels stop at order 8. Here one
+// warp owns one path: the dense 2K formulation (edges carry their zero basis
+// column, geometry.py:86-90), the inverse Hessian and the per-path vectors in
+// shared memory (row stride m + 1, so a row per lane is bank-conflict free),
+// lanes striding over interactions, segments and Hessian rows, reductions as
+// warp butterflies. The operations follow the reference's batched code in
+// order — embed / clamped segments / gradient (batching.py:83-126), the
+// fixed-point step size (solver.py:84-112), the BFGS loop with its curvature
+// and finite-H' guards (solver.py:146-215) — in fp32 or fp64, with IEEE
+// division and square root. The implicit VJP (objective.py:48-135,
+// implicit_diff.py:39-77) assembles the block-tridiagonal Hessian in parallel
+// and runs the block-Thomas solve (with the Tikhonov retry) on one lane.
+// This is the long-path fallback: correct and bounded, not the tuned path.
+#include <cuda_runtime.h>
+
+#include "fp_dispatch.h"
+#include "fp_kernels.cuh"
+
+namespace fp {
+
+namespace {
+
+constexpr int kWideMaxOrder = 64;
+constexpr int kWideThreads = 128;  // 4 paths per CTA when shared memory allows
+
+template <typename R>
+__device__ __forceinline__ R warp_sum(R v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+template <typename R>
+__device__ __forceinline__ R warp_min(R v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const R w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w < v ? w : v;
+  }
+  return v;
+}
+
+// Per-warp shared-memory layout (units of R).
+struct WideLayout {
+  int K, m, S, ld;
+  int H, t, g, gn, p, st, y, hy, A, b, x, s, nc, nu, u, d, a2c, D, O, rhs, act, sol, dx, w, red;
+  int total;
+  __host__ __device__ explicit WideLayout(int k) : K(k), m(2 * k), S(k + 1), ld(2 * k + 1) {
+    int o = 0;
+    H = o; o += m * ld;
+    t = o; o += m;
+    g = o; o += m;
+    gn = o; o += m;
+    p = o; o += m;
+    st = o; o += m;
+    y = o; o += m;
+    hy = o; o += m;
+    A = o; o += 6 * K;
+    b = o; o += 3 * K;
+    x = o; o += 3 * (K + 2);
+    s = o; o += 3 * S;
+    nc = o; o += S;
+    nu = o; o += S;
+    u = o; o += 3 * S;
+    d = o; o += 3 * S;
+    a2c = o; o += 2 * S;
+    D = o; o += 3 * K;
+    O = o; o += 4 * K;
+    rhs = o; o += 2 * K;
+    act = o; o += 2 * K;
+    sol = o; o += 2 * K;
+    dx = o; o += 3 * K;
+    w = o; o += 3 * S;
+    red = o; o += 8;
+    total = (o + 1) & ~1;  // keep every warp's block 16-byte aligned for doubles
+  }
+};
+
+template <typename R>
+struct WideCtx {
+  WideLayout L;
+  R* sm;
+  int lane;
+  R eps;
+  __device__ R* at(int off) const { return sm + off; }
+  __device__ R Aij(int i, int r, int c) const { return sm[L.A + 6 * i + 2 * r + c]; }
+};
+
+// x, segments, norms and the clamped gradient of the parameters at `t`
+// into `gout` (batching.py:83-120): einsum order, IEEE div / sqrt.
+template <typename R>
+__device__ void wide_eval(const WideCtx<R>& c, const R* t, R* gout) {
+  const WideLayout& L = c.L;
+  R* sm = c.sm;
+  for (int q = c.lane; q < L.K + 2; q += 32) {
+    R* X = sm + L.x + 3 * q;
+    if (q == 0 || q == L.K + 1) continue;  // endpoints stored at load
+    const int i = q - 1;
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+      X[r] = (c.Aij(i, r, 0) * t[2 * i] + c.Aij(i, r, 1) * t[2 * i + 1]) + sm[L.b + 3 * i + r];
+  }
+  __syncwarp();
+  for (int k = c.lane; k < L.S; k += 32) {
+    const R* lo = sm + L.x + 3 * k;
+    const R* hi = lo + 3;
+    R s[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) s[r] = hi[r] - lo[r];
+    const R n = Num<R>::sqrt_((s[0] * s[0] + s[1] * s[1]) + s[2] * s[2]);
+    const R cl = n < c.eps ? c.eps : n;  // np.maximum: NaN propagates
+    sm[L.nu + k] = n;
+    sm[L.nc + k] = cl;
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      sm[L.s + 3 * k + r] = s[r];
+      sm[L.u + 3 * k + r] = Num<R>::div(s[r], cl);
+    }
+  }
+  __syncwarp();
+  for (int i = c.lane; i < L.K; i += 32) {
+    R q[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) q[r] = sm[L.u + 3 * i + r] - sm[L.u + 3 * (i + 1) + r];
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc)
+      gout[2 * i + cc] = (c.Aij(i, 0, cc) * q[0] + c.Aij(i, 1, cc) * q[1]) + c.Aij(i, 2, cc) * q[2];
+  }
+  __syncwarp();
+}
+
+template <typename R>
+__device__ R wide_length(const WideCtx<R>& c) {
+  R l = R(0);
+  for (int k = c.lane; k < c.L.S; k += 32) l += c.sm[c.L.nu + k];
+  return warp_sum(l);
+}
+
+template <typename R>
+__device__ R wide_dot(const WideCtx<R>& c, const R* a, const R* b) {
+  R acc = R(0);
+  for (int j = c.lane; j < c.L.m; j += 32) acc = fma(a[j], b[j], acc);
+  return warp_sum(acc);
+}
+
+// out = H v (rows across lanes).
+template <typename R>
+__device__ void wide_matvec(const WideCtx<R>& c, const R* v, R* out, R sign) {
+  const WideLayout& L = c.L;
+  for (int j = c.lane; j < L.m; j += 32) {
+    const R* h = c.sm + L.H + j * L.ld;
+    R acc = R(0);
+    for (int q = 0; q < L.m; ++q) acc = fma(h[q], v[q], acc);
+    out[j] = sign * acc;
+  }
+  __syncwarp();
+}
+
+// Fixed-point step size along p (solver.py:84-112); sets `zero`.
+template <typename R>
+__device__ R wide_step_size(const WideCtx<R>& c, const R* p, int fp_iters, bool& zero) {
+  const WideLayout& L = c.L;
+  R* sm = c.sm;
+  R a2sum = R(0);
+  for (int k = c.lane; k < L.S; k += 32) {
+    R dd[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const R hi = k < L.K ? c.Aij(k, r, 0) * p[2 * k] + c.Aij(k, r, 1) * p[2 * k + 1] : R(0);
+      const R lo = k > 0 ? c.Aij(k - 1, r, 0) * p[2 * k - 2] + c.Aij(k - 1, r, 1) * p[2 * k - 1] : R(0);
+      dd[r] = hi - lo;
+      sm[L.d + 3 * k + r] = dd[r];
+    }
+    const R* s = sm + L.s + 3 * k;
+    const R a2 = (dd[0] * dd[0] + dd[1] * dd[1]) + dd[2] * dd[2];
+    const R cc = (dd[0] * s[0] + dd[1] * s[1]) + dd[2] * s[2];
+    sm[L.a2c + 2 * k] = a2;
+    sm[L.a2c + 2 * k + 1] = cc;
+    a2sum += a2;
+  }
+  zero = warp_sum(a2sum) <= Num<R>::tiny();
+  R alpha = R(0);
+  for (int f = 0; f < fp_iters; ++f) {
+    R num = R(0), den = R(0);
+    for (int k = c.lane; k < L.S; k += 32) {
+      const R* s = sm + L.s + 3 * k;
+      const R* dd = sm + L.d + 3 * k;
+      R e[3];
+#pragma unroll
+      for (int r = 0; r < 3; ++r) e[r] = s[r] + alpha * dd[r];
+      R n = Num<R>::sqrt_((e[0] * e[0] + e[1] * e[1]) + e[2] * e[2]);
+      n = n < c.eps ? c.eps : n;
+      num += Num<R>::div(sm[L.a2c + 2 * k + 1], n);
+      den += Num<R>::div(sm[L.a2c + 2 * k], n);
+    }
+    num = warp_sum(num);
+    den = warp_sum(den);
+    const R cand = -Num<R>::div(num, zero ? R(1) : den);
+    alpha = (zero || !finite(cand)) ? alpha : cand;
+  }
+  __syncwarp();
+  return alpha;
+}
+
+// Implicit VJP at the current state (same mathematics as implicit_vjp in
+// fp_path.cuh): outputs to the path's records directly.
+template <typename R>
+__device__ uint8_t wide_vjp(const WideCtx<R>& c, const PathArgs<R>& a, int64_t row, const R* t) {
+  const WideLayout& L = c.L;
+  R* sm = c.sm;
+  const int K = L.K;
+  uint8_t st = 0;
+  const R wl = a.wL ? a.wL[row] : a.wL_scale;
+  const bool full = a.mode == FP_VJP_FULL, mixed = a.mode == FP_VJP_MIXED;
+  const bool has_v = a.vT != nullptr;
+  const bool need_solve = !mixed && (has_v || (full && wl != R(0)));
+  const R* vT = has_v ? a.vT + row * 2 * K : nullptr;
+  // per interaction: active flags, Hessian blocks, rhs
+  R trace = R(0);
+  for (int i = c.lane; i < K; i += 32) {
+    bool act[2];
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {
+      act[cc] = c.Aij(i, 0, cc) != R(0) || c.Aij(i, 1, cc) != R(0) || c.Aij(i, 2, cc) != R(0);
+      sm[L.act + 2 * i + cc] = act[cc] ? R(1) : R(0);
+      const R v = vT ? vT[2 * i + cc] : R(0);
+      sm[L.sol + 2 * i + cc] = mixed ? v : R(0);
+      const R gv = full ? fma(wl, sm[L.g + 2 * i + cc], v) : v;
+      sm[L.rhs + 2 * i + cc] = act[cc] ? -gv : R(0);
+    }
+    if (!need_solve) continue;
+    const R* ui = sm + L.u + 3 * i;
+    const R* uo = ui + 3;
+    const R ri = R(1) / sm[L.nc + i], ro = R(1) / sm[L.nc + i + 1];
+    R ain[2], aout[2], gii[3];
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {
+      ain[cc] = fma(c.Aij(i, 2, cc), ui[2], fma(c.Aij(i, 1, cc), ui[1], c.Aij(i, 0, cc) * ui[0]));
+      aout[cc] = fma(c.Aij(i, 2, cc), uo[2], fma(c.Aij(i, 1, cc), uo[1], c.Aij(i, 0, cc) * uo[0]));
+    }
+    gii[0] = fma(c.Aij(i, 2, 0), c.Aij(i, 2, 0), fma(c.Aij(i, 1, 0), c.Aij(i, 1, 0), c.Aij(i, 0, 0) * c.Aij(i, 0, 0)));
+    gii[1] = fma(c.Aij(i, 2, 0), c.Aij(i, 2, 1), fma(c.Aij(i, 1, 0), c.Aij(i, 1, 1), c.Aij(i, 0, 0) * c.Aij(i, 0, 1)));
+    gii[2] = fma(c.Aij(i, 2, 1), c.Aij(i, 2, 1), fma(c.Aij(i, 1, 1), c.Aij(i, 1, 1), c.Aij(i, 0, 1) * c.Aij(i, 0, 1)));
+    R D0 = (gii[0] - ain[0] * ain[0]) * ri + (gii[0] - aout[0] * aout[0]) * ro;
+    R D1 = (gii[1] - ain[0] * ain[1]) * ri + (gii[1] - aout[0] * aout[1]) * ro;
+    R D2 = (gii[2] - ain[1] * ain[1]) * ri + (gii[2] - aout[1] * aout[1]) * ro;
+    if (act[0]) trace += D0;
+    if (act[1]) trace += D2;
+    if (!act[0]) { D0 = R(1); D1 = R(0); }
+    if (!act[1]) { D2 = R(1); D1 = R(0); }
+    sm[L.D + 3 * i] = D0;
+    sm[L.D + 3 * i + 1] = D1;
+    sm[L.D + 3 * i + 2] = D2;
+    if (i + 1 < K) {
+      R ain1[2];  // A_{i+1}^T u_{i+1}
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc)
+        ain1[cc] = fma(c.Aij(i + 1, 2, cc), uo[2], fma(c.Aij(i + 1, 1, cc), uo[1], c.Aij(i + 1, 0, cc) * uo[0]));
+#pragma unroll
+      for (int aa = 0; aa < 2; ++aa)
+#pragma unroll
+        for (int bb = 0; bb < 2; ++bb) {
+          const R gij = fma(c.Aij(i, 2, aa), c.Aij(i + 1, 2, bb),
+                            fma(c.Aij(i, 1, aa), c.Aij(i + 1, 1, bb), c.Aij(i, 0, aa) * c.Aij(i + 1, 0, bb)));
+          sm[L.O + 4 * i + 2 * aa + bb] = -(gij - aout[aa] * ain1[bb]) * ro;
+        }
+    }
+  }
+  trace = warp_sum(trace);
+  __syncwarp();
+  if (need_solve) {
+    if (c.lane == 0) {
+      // block Thomas elimination with the Tikhonov retry (implicit_diff.py:64-71);
+      // Ci and z reuse dx (3K) and w (2K of 3S) as scratch
+      R* Ci = sm + L.dx;
+      R* z = sm + L.w;
+      bool solved = false;
+      for (int attempt = 0; attempt < 2 && !solved; ++attempt) {
+        const R lam = attempt == 0 ? R(0) : R(1e-12) * trace;
+        bool ok = true;
+        for (int i = 0; i < K; ++i) {
+          const R* D = sm + L.D + 3 * i;
+          const bool a0 = sm[L.act + 2 * i] != R(0), a1 = sm[L.act + 2 * i + 1] != R(0);
+          R C0 = D[0] + (a0 ? lam : R(0)), C1 = D[1], C2 = D[2] + (a1 ? lam : R(0));
+          R z0 = sm[L.rhs + 2 * i], z1 = sm[L.rhs + 2 * i + 1];
+          if (i > 0) {
+            const R* O = sm + L.O + 4 * (i - 1);  // O[a][b] = O[2a + b]
+            const R* Cp = Ci + 3 * (i - 1);
+            R Lm[2][2];
+#pragma unroll
+            for (int aa = 0; aa < 2; ++aa) {
+              Lm[aa][0] = O[aa] * Cp[0] + O[2 + aa] * Cp[1];
+              Lm[aa][1] = O[aa] * Cp[1] + O[2 + aa] * Cp[2];
+            }
+            C0 -= Lm[0][0] * O[0] + Lm[0][1] * O[2];
+            C1 -= Lm[0][0] * O[1] + Lm[0][1] * O[3];
+            C2 -= Lm[1][0] * O[1] + Lm[1][1] * O[3];
+            z0 -= Lm[0][0] * z[2 * (i - 1)] + Lm[0][1] * z[2 * (i - 1) + 1];
+            z1 -= Lm[1][0] * z[2 * (i - 1)] + Lm[1][1] * z[2 * (i - 1) + 1];
+          }
+          const R det = C0 * C2 - C1 * C1;
+          ok = ok && det > R(0) && finite(det);
+          const R id = R(1) / det;
+          Ci[3 * i] = C2 * id;
+          Ci[3 * i + 1] = -C1 * id;
+          Ci[3 * i + 2] = C0 * id;
+          z[2 * i] = z0;
+          z[2 * i + 1] = z1;
+        }
+        if (!ok) continue;
+        R nx0 = R(0), nx1 = R(0);
+        for (int i = K - 1; i >= 0; --i) {
+          R r0 = z[2 * i], r1 = z[2 * i + 1];
+          if (i + 1 < K) {
+            const R* O = sm + L.O + 4 * i;
+            r0 -= O[0] * nx0 + O[1] * nx1;
+            r1 -= O[2] * nx0 + O[3] * nx1;
+          }
+          const R v0 = Ci[3 * i] * r0 + Ci[3 * i + 1] * r1;
+          const R v1 = Ci[3 * i + 1] * r0 + Ci[3 * i + 2] * r1;
+          nx0 = sm[L.act + 2 * i] != R(0) ? v0 : R(0);
+          nx1 = sm[L.act + 2 * i + 1] != R(0) ? v1 : R(0);
+          sm[L.sol + 2 * i] = nx0;
+          sm[L.sol + 2 * i + 1] = nx1;
+          ok = ok && finite(v0) && finite(v1);
+        }
+        solved = ok;
+      }
+      if (!solved)
+        for (int i = 0; i < 2 * K; ++i) sm[L.sol + i] = R(0);
+      sm[L.red] = solved ? R(1) : R(0);
+    }
+    __syncwarp();
+    if (sm[L.red] == R(0)) st |= FP_STATUS_SINGULAR;
+  }
+  // param_vjp with the solution + wl * length partials (objective.py:89-135)
+  for (int i = c.lane; i < K; i += 32)
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+      sm[L.dx + 3 * i + r] = fma(c.Aij(i, r, 1), sm[L.sol + 2 * i + 1], c.Aij(i, r, 0) * sm[L.sol + 2 * i]);
+  __syncwarp();
+  for (int k = c.lane; k < L.S; k += 32) {
+    const R* u = sm + L.u + 3 * k;
+    R ds[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const R hi = k < K ? sm[L.dx + 3 * k + r] : R(0);
+      const R lo = k > 0 ? sm[L.dx + 3 * (k - 1) + r] : R(0);
+      ds[r] = hi - lo;
+    }
+    const R ud = fma(u[2], ds[2], fma(u[1], ds[1], u[0] * ds[0]));
+    const R rk = R(1) / sm[L.nc + k];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) sm[L.w + 3 * k + r] = (ds[r] - u[r] * ud) * rk;
+  }
+  __syncwarp();
+  bool fin = true;
+  for (int i = c.lane; i < K; i += 32) {
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const R q = sm[L.u + 3 * i + r] - sm[L.u + 3 * (i + 1) + r];
+      const R zi = sm[L.w + 3 * i + r] - sm[L.w + 3 * (i + 1) + r];
+      const R e = fma(wl, q, zi);
+      const R b0 = fma(e, t[2 * i], q * sm[L.sol + 2 * i]);
+      const R b1 = fma(e, t[2 * i + 1], q * sm[L.sol + 2 * i + 1]);
+      fin = fin && finite(e) && finite(b0) && finite(b1);
+      if (a.d_anchor) a.d_anchor[(row * K + i) * 3 + r] = e;
+      if (a.d_basis) {
+        a.d_basis[(row * K + i) * 6 + 2 * r] = b0;
+        a.d_basis[(row * K + i) * 6 + 2 * r + 1] = b1;
+      }
+    }
+    if (a.u_out) {
+      a.u_out[(row * K + i) * 2] = sm[L.sol + 2 * i];
+      a.u_out[(row * K + i) * 2 + 1] = sm[L.sol + 2 * i + 1];
+    }
+  }
+  if (c.lane < 3) {
+    const int r = c.lane;
+    const R d0 = -fma(wl, sm[L.u + r], sm[L.w + r]);
+    const R d1 = fma(wl, sm[L.u + 3 * K + r], sm[L.w + 3 * K + r]);
+    fin = fin && finite(d0) && finite(d1);
+    if (a.d_start) a.d_start[row * 3 + r] = d0;
+    if (a.d_end) a.d_end[row * 3 + r] = d1;
+  }
+  if (!__all_sync(0xffffffffu, fin)) st |= FP_STATUS_NONFINITE;
+  return st;
+}
+
+template <typename R, int OP>
+__global__ void __launch_bounds__(kWideThreads) wide_kernel(const __grid_constant__ PathArgs<R> a, int K,
+                                                            int wpb) {
+  extern __shared__ __align__(16) unsigned char wide_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp >= wpb) return;
+  const WideLayout L(K);
+  const int64_t row = a.row_begin + int64_t(blockIdx.x) * wpb + warp;
+  if (row >= a.B) return;  // whole warp leaves together: only warp-level sync below
+  R* sm = reinterpret_cast<R*>(wide_smem) + size_t(warp) * L.total;
+  const int m = L.m;
+  // ---- load ----------------------------------------------------------------
+  for (int e = lane; e < 6 * K; e += 32) sm[L.A + e] = a.basis[row * 6 * K + e];
+  for (int e = lane; e < 3 * K; e += 32) sm[L.b + e] = a.anchor[row * 3 * K + e];
+  for (int e = lane; e < m; e += 32) sm[L.t + e] = a.T[row * m + e];
+  if (lane < 3) {
+    sm[L.x + lane] = a.start[row * 3 + lane];
+    sm[L.x + 3 * (K + 1) + lane] = a.end[row * 3 + lane];
+  }
+  __syncwarp();
+  R eps;
+  {
+    const double dx = double(sm[L.x + 3 * (K + 1)]) - double(sm[L.x]);
+    const double dy = double(sm[L.x + 3 * (K + 1) + 1]) - double(sm[L.x + 1]);
+    const double dz = double(sm[L.x + 3 * (K + 1) + 2]) - double(sm[L.x + 2]);
+    eps = R(1e-12 * (1.0 + __dsqrt_rn(__fma_rn(dz, dz, __fma_rn(dy, dy, dx * dx)))));
+  }
+  const WideCtx<R> c{L, sm, lane, eps};
+  R* t = sm + L.t;
+  R* g = sm + L.g;
+  wide_eval(c, t, g);
+  uint8_t st = 0;
+  if (OP != OP_VJP) {
+    R n0 = Num<R>::inf();
+    for (int k = lane; k < L.S; k += 32) n0 = sm[L.nu + k] < n0 ? sm[L.nu + k] : n0;
+    if (warp_min(n0) <= eps) st |= FP_STATUS_DEGENERATE_ENTRY;  // checked_segments (solver.py:166)
+    R* H = sm + L.H;
+    for (int j = lane; j < m; j += 32)
+      for (int q = 0; q < m; ++q) H[j * L.ld + q] = j == q ? R(1) : R(0);
+    R* p = sm + L.p;
+    R* stp = sm + L.st;
+    R* gn = sm + L.gn;
+    R* y = sm + L.y;
+    R* hy = sm + L.hy;
+    __syncwarp();
+    for (int it = 0; it < a.iterations; ++it) {
+      wide_matvec(c, g, p, R(-1));  // p = -H g
+      bool zero;
+      const R alpha = wide_step_size(c, p, a.fp_iters, zero);
+      if (zero) st |= FP_STATUS_ZERO_DIRECTION;
+      for (int j = lane; j < m; j += 32) {
+        stp[j] = alpha * p[j];
+        t[j] = t[j] + stp[j];
+      }
+      __syncwarp();
+      wide_eval(c, t, gn);
+      for (int j = lane; j < m; j += 32) y[j] = gn[j] - g[j];
+      __syncwarp();
+      const R sy = wide_dot(c, stp, y);
+      const R sn = Num<R>::sqrt_(wide_dot(c, stp, stp));
+      const R yn = Num<R>::sqrt_(wide_dot(c, y, y));
+      if (sy > (R(1e-12) * sn) * yn) {
+        const R rho = R(1) / sy;
+        wide_matvec(c, y, hy, R(1));
+        const R yHy = wide_dot(c, y, hy);
+        const R coef = rho * rho * yHy + rho;
+        bool fin = true;
+        for (int j = lane; j < m; j += 32) {
+          const R* h = H + j * L.ld;
+          for (int q = 0; q < m; ++q) {
+            const R v = (h[q] - rho * (stp[j] * hy[q] + stp[q] * hy[j])) + coef * (stp[j] * stp[q]);
+            fin = fin && finite(v);
+          }
+        }
+        if (__all_sync(0xffffffffu, fin)) {
+          for (int j = lane; j < m; j += 32) {
+            R* h = H + j * L.ld;
+            for (int q = 0; q < m; ++q)
+              h[q] = (h[q] - rho * (stp[j] * hy[q] + stp[q] * hy[j])) + coef * (stp[j] * stp[q]);
+          }
+        }
+        __syncwarp();
+      }
+      for (int j = lane; j < m; j += 32) g[j] = gn[j];
+      __syncwarp();
+      if (a.trace_len != nullptr) {
+        const R len = wide_length(c);
+        const R gq = wide_dot(c, g, g);
+        if (lane == 0) {
+          a.trace_len[int64_t(it) * a.ld + row] = len;
+          a.trace_gnorm[int64_t(it) * a.ld + row] = Num<R>::sqrt_(gq);
+        }
+      }
+    }
+    if (a.H_out != nullptr)
+      for (int j = lane; j < m; j += 32)
+        for (int q = 0; q < m; ++q) a.H_out[(row * m + j) * m + q] = H[j * L.ld + q];
+  }
+  // ---- final classification (as final_status) ------------------------------------
+  const R len = wide_length(c);
+  R nmin = Num<R>::inf();
+  for (int k = lane; k < L.S; k += 32) nmin = sm[L.nu + k] < nmin ? sm[L.nu + k] : nmin;
+  nmin = warp_min(nmin);
+  const R gq = wide_dot(c, g, g);
+  if (!(Num<R>::sqrt_(gq) < R(1e-5) * (R(1) + len))) st |= FP_STATUS_NOT_STATIONARY;
+  if (nmin <= eps) st |= FP_STATUS_DEGENERATE_FINAL;
+  if (nmin < R(1e-3)) st |= FP_STATUS_SHORT_SEGMENT;
+  bool fin = finite(len);
+  for (int j = lane; j < m; j += 32) fin = fin && finite(t[j]) && finite(g[j]);
+  if (!__all_sync(0xffffffffu, fin)) st |= FP_STATUS_NONFINITE;
+  if (OP != OP_VJP) {
+    for (int j = lane; j < m; j += 32) {
+      if (a.T_out) a.T_out[row * m + j] = t[j];
+      if (a.g_out) a.g_out[row * m + j] = g[j];
+    }
+    if (a.points_out)
+      for (int e = lane; e < 3 * K; e += 32) a.points_out[row * 3 * K + e] = sm[L.x + 3 + e];
+    if (a.length_out && lane == 0) a.length_out[row] = len;
+  }
+  if (OP != OP_SOLVE) st |= wide_vjp(c, a, row, t);
+  if (a.status_out && lane == 0) a.status_out[row] = st;
+}
+
+}  // namespace
+
+size_t wide_smem_per_path(int K, size_t elem) { return size_t(WideLayout(K).total) * elem; }
+
+template <typename R>
+cudaError_t dispatch_wide(int K, const PathArgs<R>& a, int op, cudaStream_t s) {
+  if (K <= 8 || K > kWideMaxOrder) return cudaErrorInvalidValue;
+  const int64_t rows = a.B - a.row_begin;
+  if (rows <= 0) return cudaSuccess;
+  const size_t per = wide_smem_per_path(K, sizeof(R));
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  int wpb = int(size_t(optin) / per);
+  wpb = wpb > kWideThreads / 32 ? kWideThreads / 32 : wpb;
+  if (wpb < 1) return cudaErrorInvalidValue;
+  const size_t smem = per * size_t(wpb);
+  const int64_t blocks = (rows + wpb - 1) / wpb;
+  const int threads = 32 * wpb;
+  cudaError_t e;
+  switch (op) {
+    case OP_SOLVE:
+      e = cudaFuncSetAttribute(wide_kernel<R, OP_SOLVE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      if (e == cudaSuccess)
+        wide_kernel<R, OP_SOLVE><<<unsigned(blocks), threads, smem, s>>>(a, K, wpb);
+      break;
+    case OP_SOLVE_VJP:
+      e = cudaFuncSetAttribute(wide_kernel<R, OP_SOLVE_VJP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(smem));
+      if (e == cudaSuccess)
+        wide_kernel<R, OP_SOLVE_VJP><<<unsigned(blocks), threads, smem, s>>>(a, K, wpb);
+      break;
+    case OP_VJP:
+      e = cudaFuncSetAttribute(wide_kernel<R, OP_VJP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      if (e == cudaSuccess) wide_kernel<R, OP_VJP><<<unsigned(blocks), threads, smem, s>>>(a, K, wpb);
+      break;
+    default:
+      return cudaErrorInvalidValue;
+  }
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+template cudaError_t dispatch_wide<float>(int, const PathArgs<float>&, int, cudaStream_t);
+template cudaError_t dispatch_wide<double>(int, const PathArgs<double>&, int, cudaStream_t);
+
+}  // namespace fp

@@ -215,6 +215,7 @@ def main():
             d[f"bfgs_T_{it}"], d[f"bfgs_g_{it}"] = r["T"], r["g"]
         out_files[f"config1_k{K}"] = d
 
+    out_files.update(wide_fixtures())
     for name, d in out_files.items():
         d = dict(d)
         d.update(meta)
@@ -223,5 +224,36 @@ def main():
     print(f"wrote {len(out_files)} fixtures, {total / 1e6:.2f} MB")
 
 
+def wide_fixtures():
+    """7. orders 9..64 (the reference's MAX_INTERACTIONS; the warp-per-path solver):
+    all-edge, all-plane and random R/D orderings, 100 iterations, fp32 + fp64,
+    implicit gradients at the fp32 solution."""
+    out = {}
+    for K in (9, 12, 16, 33, 64):
+        rng = np.random.default_rng([11, K])
+        orders = ["D" * K, "R" * K] + ["".join(rng.choice(["R", "D"], size=K)) for _ in range(4)]
+        b = datagen.gen_batch(900 + K, orders, 6)
+        arrs = (b.basis, b.anchor, b.start, b.end)
+        r32 = _fwd(arrs, b.T0, 100, 1, F32)
+        r64 = _fwd(arrs, b.T0, 100, 1, F64)
+        d = dict(basis=b.basis, anchor=b.anchor, start=b.start, end=b.end, T0=b.T0,
+                 iterations=100, fp_iters=1)
+        for k in ("T", "g", "L", "points"):
+            d[k + "_f32"] = r32[k]
+            d[k + "_f64"] = r64[k]
+        specs = _specs_from_arrays(*arrs)
+        gr = _grads_at(specs, r32["T"], np.random.default_rng([13, K]))
+        d.update({"grad_" + k: v for k, v in gr.items() if k != "hess"})
+        out[f"fwd_wide_k{K}"] = d
+    return out
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "--wide":
+        meta = dict(numpy_version=np.__version__)
+        for name, d in wide_fixtures().items():
+            d.update(meta)
+            np.savez_compressed(os.path.join(HERE, name + ".npz"), **d)
+            print("wrote", name)
+    else:
+        main()

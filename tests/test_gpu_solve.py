@@ -172,7 +172,7 @@ def test_edge_cases_empty_order0_and_errors():
     sc0 = BatchScene(np.zeros((2, 0, 3, 2)), np.zeros((2, 0, 3)), x0, x1)
     r0 = solve(sc0, None, SolveOptions(iterations=3))
     assert np.allclose(r0.length.cpu().numpy(), [5.0, 1.0])
-    big = datagen.gen_batch(1, ["R" * 9], 4)
+    big = datagen.gen_batch(1, ["R" * 65], 4)  # above MAX_INTERACTIONS (geometry.py:23)
     with pytest.raises(NotImplementedError):
         solve(BatchScene(big.basis, big.anchor, big.start, big.end), big.T0, SolveOptions(iterations=2))
     # degenerate entry: plane through the start point (test_objective.py:46-55)

@@ -156,3 +156,20 @@ def test_enumeration_oracle_self_consistent():
             got |= {tuple(s) for s in seqs}
         assert got == E.brute_force_sequences(kinds, order)
         assert len(got) == len(kinds) * (len(kinds) - 1) ** (order - 1)
+
+
+@pytest.mark.parametrize("K", [9, 16, 64])
+def test_wide_orders_forward(K):
+    """Orders 9..64 (geometry.py:23 MAX_INTERACTIONS): the oracle restatement
+    reproduces the reference there too."""
+    d = golden(f"fwd_wide_k{K}")
+    ex = _same_numpy(d)
+    for dt, suf in ((np.float32, "_f32"), (np.float64, "_f64")):
+        r = O.bfgs(d["basis"], d["anchor"], d["start"], d["end"], d["T0"], int(d["iterations"]), 1, dt)
+        conv = converged_mask(d["basis"], d["anchor"], d["start"], d["end"], d["T" + suf])
+        assert conv.sum() >= 4
+        if ex:
+            assert np.array_equal(r["T"], d["T" + suf])
+            assert np.array_equal(r["g"], d["g" + suf])
+        else:
+            assert np.allclose(r["T"][conv], d["T" + suf][conv], rtol=1e-5, atol=1e-5)
