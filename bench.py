@@ -192,10 +192,16 @@ def run_reference(args):
 
     K, I = args.order, args.iterations
     batch = datagen.config2(K, 1 << 12 if args.quick else args.sample)
-    (b, a, s0, s1, T0), n, _ = cpu_sample(batch, batch.size)
     pool = CpuPool()
-    for _ in range(args.warmup):
-        pool.run(b, a, s0, s1, T0, I)
+    # Warm-up steps on a small slice also calibrate the per-step sample: the
+    # timed steps together stay within ~150 s of CPU work whatever --steps is.
+    (b, a, s0, s1, T0), n_cal, _ = cpu_sample(batch, min(batch.size, 8192))
+    rate = None
+    for _ in range(max(1, args.warmup)):
+        c, w = pool.run(b, a, s0, s1, T0, I)
+        rate = n_cal / w
+    n_step = int(min(batch.size, max(4096, rate * 150.0 / max(1, args.steps))))
+    (b, a, s0, s1, T0), n, _ = cpu_sample(batch, n_step)
     conv_total, wall_total = 0, 0.0
     for _ in range(args.steps):
         c, w = pool.run(b, a, s0, s1, T0, I)
