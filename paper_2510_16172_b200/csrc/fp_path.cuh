@@ -544,10 +544,6 @@ __device__ __forceinline__ void bfgs_iterations(const Geo<R, K>& G, PathState<R,
   constexpr int NA = L::NA;
   constexpr int NP = Packed<NA>::NP;
   const int fp_iters = GENERAL ? fp_iters_rt : 1;
-#ifdef FP_UNROLL_ITER
-  constexpr int kUnrollIter = FP_UNROLL_ITER;
-#pragma unroll kUnrollIter
-#endif
   for (int it = 0; it < iterations; ++it) {
     bool zero;
     const R alpha = P.step_size(G, p, fp_iters, zero);
