@@ -221,20 +221,23 @@ int fp_peak_ffma(int blocks, int iters, float* out, void* stream);
 int fp_gate_wait(const int* host_flag, double timeout_s, void* stream);
 
 /* ---- bookkeeping ---------------------------------------------------------- */
-/* Kernel selection for fp32 solves / fused steps (other calls run the dense
- * kernels). Every policy runs, for each path, the kernel variant carrying only
- * its active unknowns (its interaction-kind mask), except FP_POLICY_DENSE.
- *   FP_POLICY_AUTO (default): order <= 3 runs the tile kernel (one launch; each
- *     warp dispatches on its paths' masks; no host round trip) unless the last
- *     call of that order saw more than 1/8 mixed-mask warps (a scattered
- *     layout), which then goes to the bucketed path; orders 4-5 are bucketed.
+/* Kernel selection for solves / fused steps of order 1..5 (other calls run
+ * the dense kernels of their order). Every policy but FP_POLICY_DENSE runs,
+ * for each path, the kernel variant carrying only its active unknowns (its
+ * interaction-kind mask).
+ *   FP_POLICY_AUTO (default): the tile kernel (one launch; each warp
+ *     dispatches on its paths' masks; no host round trip; fp32 and fp64)
+ *     unless the last call of that order saw more than 1/8 mixed-mask warps
+ *     (a scattered layout), which then goes to the bucketed path (fp32) or
+ *     the dense kernel (fp64).
  *   FP_POLICY_DENSE: the uniform 2K kernel for every path (agrees with the
  *     specialised variants to rounding; used by the tests).
- *   FP_POLICY_AUTO_SERIAL: bucketed, per-mask kernels one after another on
- *     the caller's stream instead of concurrent side streams.
- *   FP_POLICY_BUCKET: always bucketed (classify on the device, one host
- *     round trip, one kernel per mask over its row range or permutation).
- *   FP_POLICY_TILE: always the tile kernel for order <= 3.
+ *   FP_POLICY_AUTO_SERIAL: bucketed (fp32), per-mask kernels one after
+ *     another on the caller's stream instead of concurrent side streams.
+ *   FP_POLICY_BUCKET: always bucketed for fp32 (classify on the device, one
+ *     host round trip, one kernel per mask over its row range or
+ *     permutation).
+ *   FP_POLICY_TILE: always the tile kernel.
  * A path's results are bitwise the same under AUTO, AUTO_SERIAL, BUCKET and
  * TILE. */
 #define FP_POLICY_AUTO 0

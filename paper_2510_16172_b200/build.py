@@ -62,7 +62,7 @@ def _units(orders=ORDERS, obj_dir=None):
     for k in orders:
         parts = (0, 1, 2) if k <= SPECIALISED_MAX_ORDER else (0,)
         if k <= TILE_MAX_ORDER:
-            parts += (3,)
+            parts += (3, 4)
         for part in parts:
             units.append((inst, os.path.join(obj_dir, f"fp_inst_k{k}_p{part}.o"),
                           [f"-DFP_INST_K={k}", f"-DFP_INST_PART={part}"]))
@@ -72,7 +72,8 @@ def _units(orders=ORDERS, obj_dir=None):
         if os.path.exists(path):
             units.append((path, os.path.join(obj_dir, extra.replace(".cu", ".o")), []))
     # longest units first so the parallel build finishes sooner
-    units.sort(key=lambda u: -sum(int(d.split("=")[1]) * (4 if "FP_INST_PART=3" in " ".join(u[2]) else 1)
+    units.sort(key=lambda u: -sum(int(d.split("=")[1]) * (4 if ("FP_INST_PART=3" in " ".join(u[2]) or
+                                                             "FP_INST_PART=4" in " ".join(u[2])) else 1)
                                   for d in u[2] if "FP_INST_K" in d))
     return units
 
@@ -136,8 +137,9 @@ def build_variant(out: str, orders, defines=(), jobs=None) -> str:
                 fh.write(f"template <> cudaError_t dispatch_dense<{R}, {k}>(const PathArgs<{R}>&, int, "
                          "cudaStream_t) { return cudaErrorNotSupported; }\n")
             if k <= TILE_MAX_ORDER:
-                fh.write(f"template <> cudaError_t dispatch_tile<{k}>(const PathArgs<float>&, int, "
-                         "cudaStream_t) { return cudaErrorNotSupported; }\n")
+                for R in ("float", "double"):
+                    fh.write(f"template <> cudaError_t dispatch_tile<{R}, {k}>(const PathArgs<{R}>&, int, "
+                             "cudaStream_t) { return cudaErrorNotSupported; }\n")
             if k <= SPECIALISED_MAX_ORDER:
                 for fn in ("dispatch_masked_solve", "dispatch_masked_solve_vjp"):
                     fh.write(f"template <> cudaError_t {fn}<{k}>(const PathArgs<float>&, unsigned, "

@@ -148,8 +148,9 @@ static void record_mixed_fraction(int K, int64_t mixed, int64_t B) {
   p.pending[K] = false;
 }
 
-static cudaError_t run_tile(int K, const PathArgs<float>& a0, int op, cudaStream_t s) {
-  PathArgs<float> a = a0;
+template <typename R>
+static cudaError_t run_tile(int K, const PathArgs<R>& a0, int op, cudaStream_t s) {
+  PathArgs<R> a = a0;
   LayoutProbe& p = probe();
   cudaError_t e = cudaSuccess;
   bool probing = false;
@@ -173,11 +174,11 @@ static cudaError_t run_tile(int K, const PathArgs<float>& a0, int op, cudaStream
     }
   }
   switch (K) {
-    case 1: e = dispatch_tile<1>(a, op, s); break;
-    case 2: e = dispatch_tile<2>(a, op, s); break;
-    case 3: e = dispatch_tile<3>(a, op, s); break;
-    case 4: e = dispatch_tile<4>(a, op, s); break;
-    default: e = dispatch_tile<5>(a, op, s); break;
+    case 1: e = dispatch_tile<R, 1>(a, op, s); break;
+    case 2: e = dispatch_tile<R, 2>(a, op, s); break;
+    case 3: e = dispatch_tile<R, 3>(a, op, s); break;
+    case 4: e = dispatch_tile<R, 4>(a, op, s); break;
+    default: e = dispatch_tile<R, 5>(a, op, s); break;
   }
   count_launches(1);
   if (e == cudaSuccess && probing) {
@@ -190,13 +191,14 @@ static cudaError_t run_tile(int K, const PathArgs<float>& a0, int op, cudaStream
   return e;
 }
 
-// fp32 solve / fused step for K <= 5. Tile path (see run_tile), or bucketed:
-// classify paths by kind mask on the device, then one specialised kernel per
-// non-empty mask — the staged TMA kernel on the mask's row range when it is
-// contiguous, the gathering kernel over a row permutation otherwise — on side
-// streams so tails overlap.
+// Solve / fused step for K <= 5. Tile path (see run_tile; fp32 and fp64), or
+// bucketed (fp32): classify paths by kind mask on the device, then one
+// specialised kernel per non-empty mask (the staged TMA kernel on the mask's
+// row range when it is contiguous, the gathering kernel over a row
+// permutation otherwise) on side streams so tails overlap. fp64 batches with
+// a scattered layout run the dense kernel.
 // Routes: any kernel the policy picks; never one that synchronises the
-// stream (tile or dense — for enqueue loops like the host-buffer pipeline);
+// stream (tile or dense, for enqueue loops like the host-buffer pipeline);
 // dense only.
 enum Route { kRouteAny = 0, kRouteNoSync = 1, kRouteDense = 2 };
 
@@ -205,16 +207,16 @@ static int dispatch(int K, const PathArgs<R>& a, int op, cudaStream_t s, int rou
   constexpr bool is_f32 = sizeof(R) == sizeof(float);
   const int64_t B = a.B;
   const int policy = g_policy.load();
-  const bool bucketed = is_f32 && route != kRouteDense && policy != FP_POLICY_DENSE && K >= 1 &&
-                        K <= kMaxSpecialisedOrder && (op == OP_SOLVE || op == OP_SOLVE_VJP) &&
-                        B > 0 && B < (int64_t(1) << 31) && a.rows == nullptr;
-  if (!bucketed) return dispatch_dense_k<R>(K, a, op, s);
+  const bool special = route != kRouteDense && policy != FP_POLICY_DENSE && K >= 1 &&
+                       K <= kMaxSpecialisedOrder && (op == OP_SOLVE || op == OP_SOLVE_VJP) &&
+                       B > 0 && B < (int64_t(1) << 31) && a.rows == nullptr;
+  if (!special) return dispatch_dense_k<R>(K, a, op, s);
+  const bool tile = (K <= kMaxTileOrder && policy == FP_POLICY_TILE) ||
+                    (K <= kAutoTileMaxOrder && policy == FP_POLICY_AUTO &&
+                     (route == kRouteNoSync || tile_preferred(K)));
+  if (tile) return cuda_status(run_tile<R>(K, a, op, s));
+  if (!is_f32 || route == kRouteNoSync) return dispatch_dense_k<R>(K, a, op, s);
   if constexpr (is_f32) {
-    const bool tile = (K <= kMaxTileOrder && policy == FP_POLICY_TILE) ||
-                      (K <= kAutoTileMaxOrder && policy == FP_POLICY_AUTO &&
-                       (route == kRouteNoSync || tile_preferred(K)));
-    if (tile) return cuda_status(run_tile(K, a, op, s));
-    if (route == kRouteNoSync) return dispatch_dense_k<R>(K, a, op, s);
     BucketScratch sc;
     BucketPlan plan;
     cudaError_t e = bucket_plan<float>(a.basis, B, K, sc, plan, s);

@@ -20,9 +20,9 @@ cudaError_t dispatch_masked_solve(const PathArgs<float>& a, unsigned mask, cudaS
 template <int K>
 cudaError_t dispatch_masked_solve_vjp(const PathArgs<float>& a, unsigned mask, cudaStream_t s);
 
-// Tile kernels (per-warp kind-mask dispatch, fp32, K <= 5); fp_inst.cu part 3.
-template <int K>
-cudaError_t dispatch_tile(const PathArgs<float>& a, int op, cudaStream_t s);
+// Tile kernels (per-warp kind-mask dispatch, K <= 5); fp_inst.cu parts 3 (fp32), 4 (fp64).
+template <typename R, int K>
+cudaError_t dispatch_tile(const PathArgs<R>& a, int op, cudaStream_t s);
 
 // Warp-per-path solver for orders 9..64 (fp_wide.cu), every op, fp32/fp64.
 template <typename R>

@@ -3,8 +3,8 @@
 //   -DFP_INST_K=K -DFP_INST_PART=0   dense kernels (fp32 + fp64, every op)
 //   -DFP_INST_PART=1 / 2             kind-mask specialised fp32 solve /
 //                                    fused solve + VJP, one kernel per mask
-//   -DFP_INST_PART=3                 tile kernels (solve, fused): every mask
-//                                    inlined, per-warp dispatch
+//   -DFP_INST_PART=3 / 4             tile kernels (solve, fused), fp32 / fp64:
+//                                    every mask of the order, per-warp dispatch
 #include "fp_dispatch.h"
 #include "fp_kernels.cuh"
 
@@ -64,9 +64,15 @@ cudaError_t dispatch_masked_solve_vjp<kK>(const PathArgs<float>& a, unsigned mas
 }
 #elif FP_INST_PART == 3
 template <>
-cudaError_t dispatch_tile<kK>(const PathArgs<float>& a, int op, cudaStream_t s) {
+cudaError_t dispatch_tile<float, kK>(const PathArgs<float>& a, int op, cudaStream_t s) {
   return op == OP_SOLVE_VJP ? launch_path_impl<float, kK, kAnyMask, OP_SOLVE_VJP>(a, s)
                             : launch_path_impl<float, kK, kAnyMask, OP_SOLVE>(a, s);
+}
+#elif FP_INST_PART == 4
+template <>
+cudaError_t dispatch_tile<double, kK>(const PathArgs<double>& a, int op, cudaStream_t s) {
+  return op == OP_SOLVE_VJP ? launch_path_impl<double, kK, kAnyMask, OP_SOLVE_VJP>(a, s)
+                            : launch_path_impl<double, kK, kAnyMask, OP_SOLVE>(a, s);
 }
 #endif
 

@@ -290,12 +290,12 @@ __device__ __forceinline__ void run_path(const PathArgs<R>& a, int64_t row, cons
 // classification pass, no host round trip, one launch.
 constexpr unsigned kAnyMask = 0xFFFFFFFFu;
 
-template <int K>
-__device__ __forceinline__ unsigned rec_mask(const Rec<float, K>& in) {
+template <typename R, int K>
+__device__ __forceinline__ unsigned rec_mask(const Rec<R, K>& in) {
   unsigned m = 0;
 #pragma unroll
   for (int i = 0; i < K; ++i)
-    m |= unsigned(in.b[6 * i + 1] != 0.f || in.b[6 * i + 3] != 0.f || in.b[6 * i + 5] != 0.f) << i;
+    m |= unsigned(in.b[6 * i + 1] != R(0) || in.b[6 * i + 3] != R(0) || in.b[6 * i + 5] != R(0)) << i;
   return m;
 }
 
@@ -303,23 +303,23 @@ __device__ __forceinline__ unsigned rec_mask(const Rec<float, K>& in) {
 // function: ptxas compiles 2^K inlined solvers in one function too slowly.
 constexpr int kInlineTileMaxOrder = 3;
 
-template <int K, int OP, unsigned M>
-__device__ __noinline__ void run_variant(const PathArgs<float>& a, int64_t row, const Rec<float, K>& in,
+template <typename R, int K, int OP, unsigned M>
+__device__ __noinline__ void run_variant(const PathArgs<R>& a, int64_t row, const Rec<R, K>& in,
                                          bool has_v, int tid) {
-  run_path<float, K, M, OP>(a, row, in, has_v, tid, true);
+  run_path<R, K, M, OP>(a, row, in, has_v, tid, true);
 }
 
-template <int K, int OP, unsigned M = 0>
-__device__ __forceinline__ void run_any_mask(unsigned m, const PathArgs<float>& a, int64_t row,
-                                             const Rec<float, K>& in, bool has_v, int tid) {
+template <typename R, int K, int OP, unsigned M = 0>
+__device__ __forceinline__ void run_any_mask(unsigned m, const PathArgs<R>& a, int64_t row,
+                                             const Rec<R, K>& in, bool has_v, int tid) {
   if (m == M) {
     if constexpr (K <= kInlineTileMaxOrder)
-      run_path<float, K, M, OP>(a, row, in, has_v, tid, true);
+      run_path<R, K, M, OP>(a, row, in, has_v, tid, true);
     else
-      run_variant<K, OP, M>(a, row, in, has_v, tid);
+      run_variant<R, K, OP, M>(a, row, in, has_v, tid);
     return;
   }
-  if constexpr (M + 1 < (1u << K)) run_any_mask<K, OP, M + 1>(m, a, row, in, has_v, tid);
+  if constexpr (M + 1 < (1u << K)) run_any_mask<R, K, OP, M + 1>(m, a, row, in, has_v, tid);
 }
 
 // Copy `width`-element records of the tile from global to shared memory with
@@ -414,13 +414,13 @@ __device__ __forceinline__ void process_tile(const PathArgs<R>& a, const int32_t
   if (tid < n) {
     const int64_t row = srow ? int64_t(srow[tid]) : base + tid;
     if constexpr (MASK == kAnyMask) {
-      const unsigned m = rec_mask<K>(in);
+      const unsigned m = rec_mask<R, K>(in);
       if (a.mixed_warps != nullptr) {
         const unsigned act = __activemask();
         if (__match_any_sync(act, m) != act && (tid & 31) == __ffs(act) - 1)
           atomicAdd(a.mixed_warps, 1ull);
       }
-      run_any_mask<K, OP>(m, a, row, in, has_v, tid);
+      run_any_mask<R, K, OP>(m, a, row, in, has_v, tid);
     } else {
       run_path<R, K, MASK, OP>(a, row, in, has_v, tid, true);
     }
@@ -515,6 +515,7 @@ template <typename R, int K, unsigned MASK>
 struct LaunchMin {
   static constexpr int value =
       MASK != kAnyMask ? MinBlocks<R, Lay<K, MASK>::NA>::value
+      : sizeof(R) == 8 ? 1  // fp64: registers are pairs; no cap (as the dense fp64 kernels)
                        : (K == 1   ? FP_TILE_MIN_BLOCKS_K1
                           : K == 2 ? FP_TILE_MIN_BLOCKS_K2
                           : K == 3 ? FP_TILE_MIN_BLOCKS_K3
