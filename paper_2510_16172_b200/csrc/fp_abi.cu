@@ -215,6 +215,12 @@ static int dispatch(int K, const PathArgs<R>& a, int op, cudaStream_t s, int rou
                     (K <= kAutoTileMaxOrder && policy == FP_POLICY_AUTO &&
                      (route == kRouteNoSync || tile_preferred(K)));
   if (tile) return cuda_status(run_tile<R>(K, a, op, s));
+  if (!is_f32 && policy == FP_POLICY_AUTO && K <= kAutoTileMaxOrder) {
+    // fp64 has no bucketed path to learn the layout from: re-probe with the
+    // tile kernel every kProbeEvery calls, run dense in between.
+    static std::atomic<int> since{0};
+    if (since.fetch_add(1) % kProbeEvery == kProbeEvery - 1) return cuda_status(run_tile<R>(K, a, op, s));
+  }
   if (!is_f32 || route == kRouteNoSync) return dispatch_dense_k<R>(K, a, op, s);
   if constexpr (is_f32) {
     BucketScratch sc;
