@@ -13,6 +13,8 @@
 //      permutation and those masks run the gathering kernel.
 #include <cuda_runtime.h>
 
+#include <mutex>
+
 #include "fp_bucket.h"
 #include "fp_dispatch.h"
 
@@ -120,6 +122,8 @@ cudaError_t bucket_plan(const R* basis, int64_t B, int K, BucketScratch& sc, Buc
   if ((e = cudaMallocAsync(&sc.small, sizeof(unsigned long long) * (4 * kMaxBuckets + 1), s)) != cudaSuccess)
     return e;
   static unsigned long long* host = nullptr;  // pinned staging for the 3 x nb + 1 stats
+  static std::mutex host_mu;                  // one caller at a time reads it back
+  std::lock_guard<std::mutex> lk(host_mu);
   if (host == nullptr) {
     if ((e = cudaMallocHost(&host, sizeof(unsigned long long) * (3 * kMaxBuckets + 1))) != cudaSuccess)
       return e;
