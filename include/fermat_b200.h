@@ -109,13 +109,15 @@ int fp_solve_vjp_f32(const float* basis, const float* anchor, const float* start
                      uint8_t* status_out, void* stream);
 
 /* Same step with HOST buffers: copies in, solves + differentiates, copies
- * out, pipelined over chunks on `nstreams` internal streams; blocks until the
- * outputs are in host memory. Pinned host memory gives full PCIe bandwidth. */
+ * out, pipelined over chunks of `chunk` paths: a copy-in, a compute and a
+ * copy-out stream over a ring of `depth` (1..8) device chunk slots, so both
+ * PCIe directions stay busy; blocks until the outputs are in host memory.
+ * Pinned host memory gives full PCIe bandwidth. */
 int fp_solve_vjp_host_f32(const float* basis, const float* anchor, const float* start,
                           const float* end, const float* T0, int64_t B, int K, int iterations,
                           int fp_iters, float w_L_scale, int mode, float* T_out, float* points_out,
                           float* length_out, float* d_basis, float* d_anchor, float* d_start,
-                          float* d_end, uint8_t* status_out, int64_t chunk, int nstreams);
+                          float* d_end, uint8_t* status_out, int64_t chunk, int depth);
 
 /* ---- objective pieces: objective.path_length / gradient / hessian
  * (objective.py:34-64), unclamped norms; degenerate segments flag

@@ -98,9 +98,27 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -
             if fh.read().strip() == digest:
                 return LIB
     units = _units()
-    jobs = jobs or min(len(units), os.cpu_count() or 4)
+    flags_stamp = os.path.join(OBJ_DIR, ".flags")
+    flags = " ".join(ARCH + NVCC_FLAGS)
+    same_flags = os.path.exists(flags_stamp) and open(flags_stamp).read() == flags
+    headers = [os.path.join(d, n) for d in (CSRC, INCLUDE) for n in os.listdir(d)
+               if n.endswith((".cuh", ".h"))]
+    newest_header = max(os.path.getmtime(h) for h in headers)
+
+    def stale(unit):
+        # an object is reused only when it is newer than its source and every
+        # shared header and was compiled with the same flags
+        src, obj, _ = unit
+        return (force or not same_flags or not os.path.exists(obj) or
+                os.path.getmtime(obj) < max(os.path.getmtime(src), newest_header))
+
+    todo = [u for u in units if stale(u)]
+    jobs = jobs or max(1, min(len(todo), os.cpu_count() or 4))
     with cf.ThreadPoolExecutor(max_workers=jobs) as ex:
-        objs = list(ex.map(_compile, units))
+        list(ex.map(_compile, todo))
+    with open(flags_stamp, "w") as fh:
+        fh.write(flags)
+    objs = [u[1] for u in units]
     tmp = LIB + ".tmp"
     cmd = [nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", tmp, *objs, "-lcudart_static"]
     res = subprocess.run(cmd, capture_output=True, text=True)

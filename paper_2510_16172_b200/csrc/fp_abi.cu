@@ -6,6 +6,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <algorithm>
@@ -148,6 +149,11 @@ static void record_mixed_fraction(int K, int64_t mixed, int64_t B) {
   p.pending[K] = false;
 }
 
+__global__ void publish_counter(unsigned long long* dev, volatile unsigned long long* host) {
+  *host = *dev;
+  *dev = 0;
+}
+
 template <typename R>
 static cudaError_t run_tile(int K, const PathArgs<R>& a0, int op, cudaStream_t s) {
   PathArgs<R> a = a0;
@@ -159,8 +165,10 @@ static cudaError_t run_tile(int K, const PathArgs<R>& a0, int op, cudaStream_t s
     if (!p.init[K]) {
       if (p.host == nullptr)
         e = cudaMallocHost(&p.host, sizeof(unsigned long long) * (kMaxTileOrder + 1));
-      if (e == cudaSuccess && p.dev == nullptr)
+      if (e == cudaSuccess && p.dev == nullptr) {
         e = cudaMalloc(&p.dev, sizeof(unsigned long long) * (kMaxTileOrder + 1));
+        if (e == cudaSuccess) e = cudaMemset(p.dev, 0, sizeof(unsigned long long) * (kMaxTileOrder + 1));
+      }
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p.ev[K], cudaEventDisableTiming);
       if (e != cudaSuccess) return e;
       p.init[K] = true;
@@ -169,8 +177,7 @@ static cudaError_t run_tile(int K, const PathArgs<R>& a0, int op, cudaStream_t s
     probing = !p.pending[K] && ++p.since[K] >= kProbeEvery;
     if (probing) {
       p.since[K] = 0;
-      if ((e = cudaMemsetAsync(p.dev + K, 0, sizeof(unsigned long long), s)) != cudaSuccess) return e;
-      a.mixed_warps = p.dev + K;
+      a.mixed_warps = p.dev + K;  // zero here: publish_counter resets it
     }
   }
   switch (K) {
@@ -183,7 +190,12 @@ static cudaError_t run_tile(int K, const PathArgs<R>& a0, int op, cudaStream_t s
   count_launches(1);
   if (e == cudaSuccess && probing) {
     std::lock_guard<std::mutex> lk(p.mu);
-    e = cudaMemcpyAsync(p.host + K, p.dev + K, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
+    // A one-thread kernel stores the counter into the pinned (UVA-mapped) host
+    // slot: a device-to-host memcpy would queue behind every copy already on
+    // the copy engine (the host-buffer pipeline's outputs) and stall this stream.
+    publish_counter<<<1, 1, 0, s>>>(p.dev + K, p.host + K);
+    count_launches(1);
+    e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaEventRecord(p.ev[K], s);
     p.warps[K] = (a.B - a.row_begin + 31) / 32;
     p.pending[K] = e == cudaSuccess;
@@ -517,14 +529,66 @@ __global__ void init_params_kernel(const R* basis, const R* anchor, const R* sta
 }
 
 // ---- host-buffer pipeline for the fused step ---------------------------------
+// Three streams: copy-in, compute, copy-out. A ring of `depth` chunk slots,
+// each with an input region and an output region on the device; cross-stream
+// events order only what shares memory:
+//   copy-in  of chunk c  waits for the kernel of chunk c - depth (input region free)
+//   kernel   of chunk c  waits for its copy-in and for the copy-out of c - depth
+//   copy-out of chunk c  waits for its kernel
+// so host-to-device copies run ahead of the device-to-host ones instead of
+// queueing behind them (one stream per slot serialises the two directions).
 struct HostPipe {
   std::mutex mu;
-  std::vector<cudaStream_t> streams;
+  cudaStream_t s_in = nullptr, s_k = nullptr, s_out = nullptr;
+  std::vector<cudaEvent_t> ev_in, ev_k, ev_out;
   std::vector<void*> bufs;
   size_t buf_bytes = 0;
   int device = -1;
+  void release() {
+    for (void* p : bufs) cudaFree(p);
+    for (auto* v : {&ev_in, &ev_k, &ev_out})
+      for (cudaEvent_t e : *v) cudaEventDestroy(e);
+    for (cudaStream_t s : {s_in, s_k, s_out})
+      if (s) cudaStreamDestroy(s);
+    bufs.clear();
+    ev_in.clear();
+    ev_k.clear();
+    ev_out.clear();
+    s_in = s_k = s_out = nullptr;
+    buf_bytes = 0;
+    device = -1;
+  }
+  cudaError_t setup(int dev, int depth, size_t slot) {
+    release();
+    cudaError_t e;
+    for (cudaStream_t* s : {&s_in, &s_k, &s_out})
+      if ((e = cudaStreamCreateWithFlags(s, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    for (int i = 0; i < depth; ++i) {
+      for (auto* v : {&ev_in, &ev_k, &ev_out}) {
+        cudaEvent_t ev;
+        if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return e;
+        v->push_back(ev);
+      }
+      void* p = nullptr;
+      if ((e = cudaMalloc(&p, slot)) != cudaSuccess) return e;
+      bufs.push_back(p);
+    }
+    buf_bytes = slot;
+    device = dev;
+    return cudaSuccess;
+  }
 };
 static HostPipe g_pipe;
+
+// The copies of one chunk in one direction, one cudaMemcpyAsync per array.
+static cudaError_t copy_arrays(void** dst, void** src, size_t* bytes, size_t n, cudaMemcpyKind kind,
+                               cudaStream_t s) {
+  for (size_t i = 0; i < n; ++i) {
+    cudaError_t e = cudaMemcpyAsync(dst[i], src[i], bytes[i], kind, s);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
 
 }  // namespace fp
 
@@ -578,8 +642,8 @@ int fp_solve_vjp_host_f32(const float* basis, const float* anchor, const float* 
                           const float* end, const float* T0, int64_t B, int K, int iterations,
                           int fp_iters, float w_L_scale, int mode, float* T_out, float* points_out,
                           float* length_out, float* d_basis, float* d_anchor, float* d_start,
-                          float* d_end, uint8_t* status_out, int64_t chunk, int nstreams) {
-  if (B < 0 || iterations < 1 || fp_iters < 1 || nstreams < 1 || nstreams > 8)
+                          float* d_end, uint8_t* status_out, int64_t chunk, int depth) {
+  if (B < 0 || iterations < 1 || fp_iters < 1 || depth < 1 || depth > 8)
     return FP_ERR_INVALID_ARGUMENT;
   if (K < 0 || K > FP_MAX_ORDER) return FP_ERR_UNSUPPORTED_ORDER;
   if (B == 0) return FP_OK;
@@ -589,34 +653,24 @@ int fp_solve_vjp_host_f32(const float* basis, const float* anchor, const float* 
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_status(e);
-  // Per-stream slot: inputs then outputs for `chunk` paths, 256-byte aligned pieces.
+  // Per slot: inputs then outputs for `chunk` paths, 256-byte aligned pieces.
   const int64_t w_in[5] = {6 * K, 3 * K, 3, 3, 2 * K};
   const int64_t w_out[7] = {2 * K, 3 * K, 1, 6 * K, 3 * K, 3, 3};
   auto al = [](size_t x) { return (x + 255) / 256 * 256; };
   size_t slot = al(size_t(chunk));  // status
   for (int i = 0; i < 5; ++i) slot += al(size_t(chunk * w_in[i]) * sizeof(float));
   for (int i = 0; i < 7; ++i) slot += al(size_t(chunk * w_out[i]) * sizeof(float));
-  if (g_pipe.device != dev || int(g_pipe.streams.size()) < nstreams || g_pipe.buf_bytes < slot) {
-    for (void* p : g_pipe.bufs) cudaFree(p);
-    for (cudaStream_t s : g_pipe.streams) cudaStreamDestroy(s);
-    g_pipe.bufs.clear();
-    g_pipe.streams.clear();
-    for (int i = 0; i < nstreams; ++i) {
-      cudaStream_t s;
-      if ((e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)) != cudaSuccess) return cuda_status(e);
-      g_pipe.streams.push_back(s);
-      void* p = nullptr;
-      if ((e = cudaMalloc(&p, slot)) != cudaSuccess) return cuda_status(e);
-      g_pipe.bufs.push_back(p);
+  if (g_pipe.device != dev || int(g_pipe.bufs.size()) != depth || g_pipe.buf_bytes < slot) {
+    if ((e = g_pipe.setup(dev, depth, slot)) != cudaSuccess) {
+      g_pipe.release();
+      return cuda_status(e);
     }
-    g_pipe.buf_bytes = slot;
-    g_pipe.device = dev;
   }
   const float* hin[5] = {basis, anchor, start, end, T0};
   float* hout[7] = {T_out, points_out, length_out, d_basis, d_anchor, d_start, d_end};
-  // Chunk schedule: ramp up from chunk/8 (the device-to-host stream, the
-  // bottleneck, starts after one small copy-in + solve instead of a full one)
-  // and back down at the end (short drain); full chunks in between.
+  // Chunk schedule: ramp up from chunk/8 (the first copy-out starts after one
+  // small copy-in + solve) and back down at the end (short drain); full
+  // chunks in between.
   std::vector<int64_t> sizes;
   {
     const int64_t r[3] = {chunk / 8, chunk / 4, chunk / 2};
@@ -635,11 +689,11 @@ int fp_solve_vjp_host_f32(const float* basis, const float* anchor, const float* 
     for (; left > 0; left -= std::min(left, chunk)) sizes.push_back(std::min(left, chunk));
     sizes.insert(sizes.end(), tail.rbegin(), tail.rend());
   }
+  cudaStream_t s_in = g_pipe.s_in, s_k = g_pipe.s_k, s_out = g_pipe.s_out;
   int64_t c = 0, lo = 0;
   for (const int64_t n : sizes) {
-    const int si = int(c % nstreams);
-    cudaStream_t s = g_pipe.streams[si];
-    char* p = static_cast<char*>(g_pipe.bufs[si]);
+    const int j = int(c % depth);
+    char* p = static_cast<char*>(g_pipe.bufs[j]);
     float* din[5];
     float* dout[7];
     for (int i = 0; i < 5; ++i) {
@@ -651,12 +705,26 @@ int fp_solve_vjp_host_f32(const float* basis, const float* anchor, const float* 
       p += al(size_t(chunk * w_out[i]) * sizeof(float));
     }
     uint8_t* dst = reinterpret_cast<uint8_t*>(p);
-    for (int i = 0; i < 5; ++i) {
-      if (w_in[i] == 0 || hin[i] == nullptr) continue;
-      e = cudaMemcpyAsync(din[i], hin[i] + lo * w_in[i], size_t(n * w_in[i]) * sizeof(float),
-                          cudaMemcpyHostToDevice, s);
-      if (e != cudaSuccess) return cuda_status(e);
+    // copy in (the slot's input region is free once chunk c - depth's kernel ran)
+    if (c >= depth && (e = cudaStreamWaitEvent(s_in, g_pipe.ev_k[j], 0)) != cudaSuccess)
+      return cuda_status(e);
+    {
+      void *dv[5], *sv[5];
+      size_t nb[5], m = 0;
+      for (int i = 0; i < 5; ++i) {
+        if (w_in[i] == 0 || hin[i] == nullptr) continue;
+        dv[m] = din[i];
+        sv[m] = const_cast<float*>(hin[i] + lo * w_in[i]);
+        nb[m++] = size_t(n * w_in[i]) * sizeof(float);
+      }
+      if ((e = copy_arrays(dv, sv, nb, m, cudaMemcpyHostToDevice, s_in)) != cudaSuccess)
+        return cuda_status(e);
     }
+    if ((e = cudaEventRecord(g_pipe.ev_in[j], s_in)) != cudaSuccess) return cuda_status(e);
+    // solve + VJP (the output region is free once chunk c - depth was copied out)
+    if ((e = cudaStreamWaitEvent(s_k, g_pipe.ev_in[j], 0)) != cudaSuccess) return cuda_status(e);
+    if (c >= depth && (e = cudaStreamWaitEvent(s_k, g_pipe.ev_out[j], 0)) != cudaSuccess)
+      return cuda_status(e);
     // Tile kernel (no host round trip): the bucketed plan would synchronise
     // its stream and stall this enqueue loop.
     int rc = solve_vjp_impl<float>(din[0], din[1], din[2], din[3], din[4], n, K, iterations, fp_iters,
@@ -664,23 +732,34 @@ int fp_solve_vjp_host_f32(const float* basis, const float* anchor, const float* 
                                    hout[1] ? dout[1] : nullptr, hout[2] ? dout[2] : nullptr,
                                    hout[3] ? dout[3] : nullptr, hout[4] ? dout[4] : nullptr,
                                    hout[5] ? dout[5] : nullptr, hout[6] ? dout[6] : nullptr,
-                                   status_out ? dst : nullptr, s, kRouteNoSync);
+                                   status_out ? dst : nullptr, s_k, kRouteNoSync);
     if (rc != FP_OK) return rc;
-    for (int i = 0; i < 7; ++i) {
-      if (w_out[i] == 0 || hout[i] == nullptr) continue;
-      e = cudaMemcpyAsync(hout[i] + lo * w_out[i], dout[i], size_t(n * w_out[i]) * sizeof(float),
-                          cudaMemcpyDeviceToHost, s);
-      if (e != cudaSuccess) return cuda_status(e);
+    if ((e = cudaEventRecord(g_pipe.ev_k[j], s_k)) != cudaSuccess) return cuda_status(e);
+    // copy out
+    if ((e = cudaStreamWaitEvent(s_out, g_pipe.ev_k[j], 0)) != cudaSuccess) return cuda_status(e);
+    {
+      void *dv[8], *sv[8];
+      size_t nb[8], m = 0;
+      for (int i = 0; i < 7; ++i) {
+        if (w_out[i] == 0 || hout[i] == nullptr) continue;
+        dv[m] = hout[i] + lo * w_out[i];
+        sv[m] = dout[i];
+        nb[m++] = size_t(n * w_out[i]) * sizeof(float);
+      }
+      if (status_out) {
+        dv[m] = status_out + lo;
+        sv[m] = dst;
+        nb[m++] = size_t(n);
+      }
+      if ((e = copy_arrays(dv, sv, nb, m, cudaMemcpyDeviceToHost, s_out)) != cudaSuccess)
+        return cuda_status(e);
     }
-    if (status_out) {
-      e = cudaMemcpyAsync(status_out + lo, dst, size_t(n), cudaMemcpyDeviceToHost, s);
-      if (e != cudaSuccess) return cuda_status(e);
-    }
+    if ((e = cudaEventRecord(g_pipe.ev_out[j], s_out)) != cudaSuccess) return cuda_status(e);
     lo += n;
     ++c;
   }
-  for (int i = 0; i < nstreams; ++i) {
-    e = cudaStreamSynchronize(g_pipe.streams[i]);
+  for (cudaStream_t s : {s_in, s_k, s_out}) {
+    e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return cuda_status(e);
   }
   return FP_OK;

@@ -162,12 +162,12 @@ def solve_with_gradients(scene: BatchScene, T0=None, opts: SolveOptions = SolveO
 
 def solve_with_gradients_host(basis, anchor, start, end, T0=None, iterations: int = 20,
                               fixed_point_iters: int = 1, weight: float = 1.0, mode: str = "full",
-                              chunk: int = 1 << 19, streams: int = 3, out=None):
+                              chunk: int = 1 << 19, depth: int = 3, out=None):
     """solve_with_gradients for host (numpy) arrays in the reference layout, fp32.
 
     One call of fp_solve_vjp_host_f32: the batch streams through the GPU in
-    chunks (copy in, fused solve + VJP, copy out on rotating streams), so host
-    transfers overlap compute. Pinned (page-locked) arrays transfer fastest:
+    chunks (copy-in, compute and copy-out streams over a ring of `depth`
+    device chunk slots), so both PCIe directions and compute overlap. Pinned (page-locked) arrays transfer fastest:
     pass `out` from `host_buffers` to reuse pinned outputs. Returns a dict of
     numpy arrays: T, points, length, status, d_basis, d_anchor, d_start, d_end.
     """
@@ -189,7 +189,7 @@ def solve_with_gradients_host(basis, anchor, start, end, T0=None, iterations: in
                                    fixed_point_iters, float(weight), _MODES[mode], P(out["T"]),
                                    P(out["points"]), P(out["length"]), P(out["d_basis"]),
                                    P(out["d_anchor"]), P(out["d_start"]), P(out["d_end"]),
-                                   P(out["status"]), int(chunk), int(streams))
+                                   P(out["status"]), int(chunk), int(depth))
     _lib.check(rc, "fp_solve_vjp_host_f32")
     return out
 

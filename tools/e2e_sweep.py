@@ -12,7 +12,7 @@ for t, a in zip(hin, (host.basis, host.anchor, host.start, host.end, host.T0)):
 hout = [pin((B, K, 2)), pin((B, K, 3)), pin((B,)), pin((B, K, 3, 2)), pin((B, K, 3)), pin((B, 3)), pin((B, 3)), pin((B,), torch.uint8)]
 P = lambda t: t.data_ptr()
 for chunk in (1 << 17, 1 << 18, 1 << 19, 1 << 20):
-    for ns in (2, 3, 4):
+    for ns in (2, 3, 4, 6):
         f = lambda: lib.fp_solve_vjp_host_f32(*(P(t) for t in hin), B, K, 20, 1, 1.0, 0, *(P(t) for t in hout), chunk, ns)
         f()
         t0 = time.perf_counter()
