@@ -143,17 +143,20 @@ def test_fused_step_equals_solve_then_vjp_bitwise():
 @pytest.mark.parametrize("K,chunk", [(3, 1024), (5, 512), (6, 256), (1, 1 << 19)])
 def test_host_pipeline_equals_device_step(K, chunk):
     """fp_solve_vjp_host_f32 (chunked host-buffer pipeline, ramped chunk sizes,
-    pinned and pageable buffers) returns the device-buffer fused step's bits."""
+    pinned and pageable buffers, ring depths 1-3) returns the device-buffer
+    fused step's bits."""
     from paper_2510_16172_b200.solver import host_buffers, solve_with_gradients_host
 
     orders = datagen.all_orderings(K) if K <= 3 else datagen.all_orderings(K)[: 6]
     b = datagen.gen_batch(60 + K, orders, 1700 // len(orders) + 3)  # ragged vs the chunk
     sc = BatchScene(b.basis, b.anchor, b.start, b.end)
     res, grads = solve_with_gradients(sc, b.T0, SolveOptions(iterations=20, precision=Precision.SINGLE))
-    for pinned in (True, False):
+    # depth 1 and 2: every chunk reuses a slot whose copy-out may still be in flight
+    for pinned, depth in ((True, 3), (False, 3), (True, 1), (True, 2)):
         out = solve_with_gradients_host(b.basis, b.anchor, b.start, b.end, b.T0, iterations=20,
-                                        chunk=chunk, out=host_buffers(b.size, K, pinned=pinned))
+                                        chunk=chunk, depth=depth,
+                                        out=host_buffers(b.size, K, pinned=pinned))
         for name, dev in (("T", res.T), ("points", res.points), ("length", res.length),
                           ("status", res.status), ("d_basis", grads.basis), ("d_anchor", grads.anchor),
                           ("d_start", grads.start), ("d_end", grads.end)):
-            assert np.array_equal(out[name], dev.cpu().numpy()), (name, pinned)
+            assert np.array_equal(out[name], dev.cpu().numpy()), (name, pinned, depth)
