@@ -107,6 +107,12 @@ int fp_solve_vjp_f32(const float* basis, const float* anchor, const float* start
                      float* T_out, float* points_out, float* length_out,
                      float* d_basis, float* d_anchor, float* d_start, float* d_end,
                      uint8_t* status_out, void* stream);
+int fp_solve_vjp_f64(const double* basis, const double* anchor, const double* start,
+                     const double* end, const double* T0, int64_t B, int K, int iterations,
+                     int fp_iters, const double* w_L, double w_L_scale, int mode,
+                     double* T_out, double* points_out, double* length_out,
+                     double* d_basis, double* d_anchor, double* d_start, double* d_end,
+                     uint8_t* status_out, void* stream);
 
 /* Same step with HOST buffers: copies in, solves + differentiates, copies
  * out, pipelined over chunks of `chunk` paths: a copy-in, a compute and a
@@ -118,6 +124,12 @@ int fp_solve_vjp_host_f32(const float* basis, const float* anchor, const float* 
                           int fp_iters, float w_L_scale, int mode, float* T_out, float* points_out,
                           float* length_out, float* d_basis, float* d_anchor, float* d_start,
                           float* d_end, uint8_t* status_out, int64_t chunk, int depth);
+int fp_solve_vjp_host_f64(const double* basis, const double* anchor, const double* start,
+                          const double* end, const double* T0, int64_t B, int K, int iterations,
+                          int fp_iters, double w_L_scale, int mode, double* T_out,
+                          double* points_out, double* length_out, double* d_basis,
+                          double* d_anchor, double* d_start, double* d_end, uint8_t* status_out,
+                          int64_t chunk, int depth);
 
 /* ---- objective pieces: objective.path_length / gradient / hessian
  * (objective.py:34-64), unclamped norms; degenerate segments flag
@@ -230,15 +242,16 @@ int fp_gate_wait(const int* host_flag, double timeout_s, void* stream);
  *   FP_POLICY_AUTO (default): the tile kernel (one launch; each warp
  *     dispatches on its paths' masks; no host round trip; fp32 and fp64)
  *     unless the last call of that order saw more than 1/8 mixed-mask warps
- *     (a scattered layout), which then goes to the bucketed path (fp32) or
- *     the dense kernel (fp64).
+ *     (a scattered layout), which then goes to the bucketed path (fp32: one
+ *     kernel per mask; fp64: the tile kernel over a mask-sorted row
+ *     permutation).
  *   FP_POLICY_DENSE: the uniform 2K kernel for every path (agrees with the
  *     specialised variants to rounding; used by the tests).
- *   FP_POLICY_AUTO_SERIAL: bucketed (fp32), per-mask kernels one after
+ *   FP_POLICY_AUTO_SERIAL: bucketed, per-mask kernels (fp32) one after
  *     another on the caller's stream instead of concurrent side streams.
- *   FP_POLICY_BUCKET: always bucketed for fp32 (classify on the device, one
- *     host round trip, one kernel per mask over its row range or
- *     permutation).
+ *   FP_POLICY_BUCKET: always bucketed (classify on the device, one host
+ *     round trip; fp32: one kernel per mask over its row range or
+ *     permutation; fp64: the tile kernel over the mask-sorted permutation).
  *   FP_POLICY_TILE: always the tile kernel.
  * A path's results are bitwise the same under AUTO, AUTO_SERIAL, BUCKET and
  * TILE. */

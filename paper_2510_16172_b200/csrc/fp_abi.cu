@@ -111,9 +111,12 @@ constexpr int kMaxTileOrder = 5;
 constexpr int kAutoTileMaxOrder = FP_AUTO_TILE_MAX_ORDER;  // orders AUTO sends to the tile kernel
 constexpr double kMaxMixedFraction = 0.125;
 
-// Re-probe the layout every kProbeEvery tile calls of an order (the other
-// calls launch the kernel alone).
-constexpr int kProbeEvery = 16;
+// Probe the layout on every tile call of an order whose previous probe has
+// come back (a counter the kernel bumps per mixed-mask warp, read back by a
+// one-thread kernel): a change to a scattered layout costs one divergent
+// call, not up to kProbeEvery of them (fp64 order 5: ~30x the sorted time
+// each). Calls enqueued while a probe is in flight launch the kernel alone.
+constexpr int kProbeEvery = 1;
 
 struct LayoutProbe {
   std::mutex mu;
@@ -174,7 +177,8 @@ static cudaError_t run_tile(int K, const PathArgs<R>& a0, int op, cudaStream_t s
       p.init[K] = true;
       p.since[K] = kProbeEvery;
     }
-    probing = !p.pending[K] && ++p.since[K] >= kProbeEvery;
+    // (a permuted launch says nothing about the caller's layout: no probe)
+    probing = a.rows == nullptr && !p.pending[K] && ++p.since[K] >= kProbeEvery;
     if (probing) {
       p.since[K] = 0;
       a.mixed_warps = p.dev + K;  // zero here: publish_counter resets it
@@ -227,13 +231,29 @@ static int dispatch(int K, const PathArgs<R>& a, int op, cudaStream_t s, int rou
                     (K <= kAutoTileMaxOrder && policy == FP_POLICY_AUTO &&
                      (route == kRouteNoSync || tile_preferred(K)));
   if (tile) return cuda_status(run_tile<R>(K, a, op, s));
-  if (!is_f32 && policy == FP_POLICY_AUTO && K <= kAutoTileMaxOrder) {
-    // fp64 has no bucketed path to learn the layout from: re-probe with the
-    // tile kernel every kProbeEvery calls, run dense in between.
-    static std::atomic<int> since{0};
-    if (since.fetch_add(1) % kProbeEvery == kProbeEvery - 1) return cuda_status(run_tile<R>(K, a, op, s));
+  if (route == kRouteNoSync || K > kMaxTileOrder) return dispatch_dense_k<R>(K, a, op, s);
+  if constexpr (!is_f32) {
+    // fp64 scattered layout (or a bucketed policy): classify, sort the rows
+    // by kind mask, and run the tile kernel over that permutation, so warps
+    // are uniform and each path still runs its own mask's variant (bitwise
+    // what the tile kernel gives it in any layout; never the dense kernel,
+    // whose rounding differs).
+    BucketScratch sc;
+    BucketPlan plan;
+    cudaError_t e = bucket_plan<R>(a.basis, B, K, sc, plan, s);
+    if (e == cudaSuccess) record_mixed_fraction(K, plan.mixed_warps, B);
+    if (e == cudaSuccess && !plan.all_contiguous) e = bucket_scatter(B, plan, sc, s);
+    if (e == cudaSuccess) {
+      PathArgs<R> b = a;
+      if (!plan.all_contiguous) {
+        b.rows = sc.rows;
+        b.n_rows = B;
+      }
+      e = run_tile<R>(K, b, op, s);
+    }
+    bucket_free(sc, s);
+    return cuda_status(e);
   }
-  if (!is_f32 || route == kRouteNoSync) return dispatch_dense_k<R>(K, a, op, s);
   if constexpr (is_f32) {
     BucketScratch sc;
     BucketPlan plan;
@@ -590,6 +610,133 @@ static cudaError_t copy_arrays(void** dst, void** src, size_t* bytes, size_t n, 
   return cudaSuccess;
 }
 
+template <typename R>
+static int host_pipeline(const R* basis, const R* anchor, const R* start, const R* end, const R* T0,
+                         int64_t B, int K, int iterations, int fp_iters, R w_L_scale, int mode,
+                         R* T_out, R* points_out, R* length_out, R* d_basis, R* d_anchor,
+                         R* d_start, R* d_end, uint8_t* status_out, int64_t chunk, int depth) {
+  if (B < 0 || iterations < 1 || fp_iters < 1 || depth < 1 || depth > 8)
+    return FP_ERR_INVALID_ARGUMENT;
+  if (K < 0 || K > FP_MAX_ORDER) return FP_ERR_UNSUPPORTED_ORDER;
+  if (B == 0) return FP_OK;
+  if (chunk <= 0) chunk = 1 << 18;
+  chunk = (chunk + kThreads - 1) / kThreads * kThreads;
+  std::lock_guard<std::mutex> lock(g_pipe.mu);
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_status(e);
+  // Per slot: inputs then outputs for `chunk` paths, 256-byte aligned pieces.
+  const int64_t w_in[5] = {6 * K, 3 * K, 3, 3, 2 * K};
+  const int64_t w_out[7] = {2 * K, 3 * K, 1, 6 * K, 3 * K, 3, 3};
+  auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+  size_t slot = al(size_t(chunk));  // status
+  for (int i = 0; i < 5; ++i) slot += al(size_t(chunk * w_in[i]) * sizeof(R));
+  for (int i = 0; i < 7; ++i) slot += al(size_t(chunk * w_out[i]) * sizeof(R));
+  if (g_pipe.device != dev || int(g_pipe.bufs.size()) != depth || g_pipe.buf_bytes < slot) {
+    if ((e = g_pipe.setup(dev, depth, slot)) != cudaSuccess) {
+      g_pipe.release();
+      return cuda_status(e);
+    }
+  }
+  const R* hin[5] = {basis, anchor, start, end, T0};
+  R* hout[7] = {T_out, points_out, length_out, d_basis, d_anchor, d_start, d_end};
+  // Chunk schedule: ramp up from chunk/8 (the first copy-out starts after one
+  // small copy-in + solve) and back down at the end (short drain); full
+  // chunks in between.
+  std::vector<int64_t> sizes;
+  {
+    const int64_t r[3] = {chunk / 8, chunk / 4, chunk / 2};
+    std::vector<int64_t> head, tail;
+    int64_t left = B;
+    for (int i = 0; i < 3 && left > 0; ++i) {
+      const int64_t h = std::min<int64_t>((r[i] + kThreads - 1) / kThreads * kThreads, left);
+      head.push_back(h);
+      left -= h;
+      if (left <= 0) break;
+      const int64_t t = std::min<int64_t>((r[i] + kThreads - 1) / kThreads * kThreads, left);
+      tail.push_back(t);
+      left -= t;
+    }
+    sizes = head;
+    for (; left > 0; left -= std::min(left, chunk)) sizes.push_back(std::min(left, chunk));
+    sizes.insert(sizes.end(), tail.rbegin(), tail.rend());
+  }
+  cudaStream_t s_in = g_pipe.s_in, s_k = g_pipe.s_k, s_out = g_pipe.s_out;
+  int64_t c = 0, lo = 0;
+  for (const int64_t n : sizes) {
+    const int j = int(c % depth);
+    char* p = static_cast<char*>(g_pipe.bufs[j]);
+    R* din[5];
+    R* dout[7];
+    for (int i = 0; i < 5; ++i) {
+      din[i] = reinterpret_cast<R*>(p);
+      p += al(size_t(chunk * w_in[i]) * sizeof(R));
+    }
+    for (int i = 0; i < 7; ++i) {
+      dout[i] = reinterpret_cast<R*>(p);
+      p += al(size_t(chunk * w_out[i]) * sizeof(R));
+    }
+    uint8_t* dst = reinterpret_cast<uint8_t*>(p);
+    // copy in (the slot's input region is free once chunk c - depth's kernel ran)
+    if (c >= depth && (e = cudaStreamWaitEvent(s_in, g_pipe.ev_k[j], 0)) != cudaSuccess)
+      return cuda_status(e);
+    {
+      void *dv[5], *sv[5];
+      size_t nb[5], m = 0;
+      for (int i = 0; i < 5; ++i) {
+        if (w_in[i] == 0 || hin[i] == nullptr) continue;
+        dv[m] = din[i];
+        sv[m] = const_cast<R*>(hin[i] + lo * w_in[i]);
+        nb[m++] = size_t(n * w_in[i]) * sizeof(R);
+      }
+      if ((e = copy_arrays(dv, sv, nb, m, cudaMemcpyHostToDevice, s_in)) != cudaSuccess)
+        return cuda_status(e);
+    }
+    if ((e = cudaEventRecord(g_pipe.ev_in[j], s_in)) != cudaSuccess) return cuda_status(e);
+    // solve + VJP (the output region is free once chunk c - depth was copied out)
+    if ((e = cudaStreamWaitEvent(s_k, g_pipe.ev_in[j], 0)) != cudaSuccess) return cuda_status(e);
+    if (c >= depth && (e = cudaStreamWaitEvent(s_k, g_pipe.ev_out[j], 0)) != cudaSuccess)
+      return cuda_status(e);
+    // Tile kernel (no host round trip): the bucketed plan would synchronise
+    // its stream and stall this enqueue loop.
+    int rc = solve_vjp_impl<R>(din[0], din[1], din[2], din[3], din[4], n, K, iterations, fp_iters,
+                                   nullptr, w_L_scale, mode, hout[0] ? dout[0] : nullptr,
+                                   hout[1] ? dout[1] : nullptr, hout[2] ? dout[2] : nullptr,
+                                   hout[3] ? dout[3] : nullptr, hout[4] ? dout[4] : nullptr,
+                                   hout[5] ? dout[5] : nullptr, hout[6] ? dout[6] : nullptr,
+                                   status_out ? dst : nullptr, s_k, kRouteNoSync);
+    if (rc != FP_OK) return rc;
+    if ((e = cudaEventRecord(g_pipe.ev_k[j], s_k)) != cudaSuccess) return cuda_status(e);
+    // copy out
+    if ((e = cudaStreamWaitEvent(s_out, g_pipe.ev_k[j], 0)) != cudaSuccess) return cuda_status(e);
+    {
+      void *dv[8], *sv[8];
+      size_t nb[8], m = 0;
+      for (int i = 0; i < 7; ++i) {
+        if (w_out[i] == 0 || hout[i] == nullptr) continue;
+        dv[m] = hout[i] + lo * w_out[i];
+        sv[m] = dout[i];
+        nb[m++] = size_t(n * w_out[i]) * sizeof(R);
+      }
+      if (status_out) {
+        dv[m] = status_out + lo;
+        sv[m] = dst;
+        nb[m++] = size_t(n);
+      }
+      if ((e = copy_arrays(dv, sv, nb, m, cudaMemcpyDeviceToHost, s_out)) != cudaSuccess)
+        return cuda_status(e);
+    }
+    if ((e = cudaEventRecord(g_pipe.ev_out[j], s_out)) != cudaSuccess) return cuda_status(e);
+    lo += n;
+    ++c;
+  }
+  for (cudaStream_t s : {s_in, s_k, s_out}) {
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_status(e);
+  }
+  return FP_OK;
+}
+
 }  // namespace fp
 
 using namespace fp;
@@ -638,131 +785,35 @@ int fp_solve_vjp_f32(const float* basis, const float* anchor, const float* start
                                d_start, d_end, status_out, static_cast<cudaStream_t>(stream));
 }
 
+int fp_solve_vjp_f64(const double* basis, const double* anchor, const double* start,
+                     const double* end, const double* T0, int64_t B, int K, int iterations,
+                     int fp_iters, const double* w_L, double w_L_scale, int mode, double* T_out,
+                     double* points_out, double* length_out, double* d_basis, double* d_anchor,
+                     double* d_start, double* d_end, uint8_t* status_out, void* stream) {
+  return solve_vjp_impl<double>(basis, anchor, start, end, T0, B, K, iterations, fp_iters, w_L,
+                                w_L_scale, mode, T_out, points_out, length_out, d_basis, d_anchor,
+                                d_start, d_end, status_out, static_cast<cudaStream_t>(stream));
+}
+
 int fp_solve_vjp_host_f32(const float* basis, const float* anchor, const float* start,
                           const float* end, const float* T0, int64_t B, int K, int iterations,
                           int fp_iters, float w_L_scale, int mode, float* T_out, float* points_out,
                           float* length_out, float* d_basis, float* d_anchor, float* d_start,
                           float* d_end, uint8_t* status_out, int64_t chunk, int depth) {
-  if (B < 0 || iterations < 1 || fp_iters < 1 || depth < 1 || depth > 8)
-    return FP_ERR_INVALID_ARGUMENT;
-  if (K < 0 || K > FP_MAX_ORDER) return FP_ERR_UNSUPPORTED_ORDER;
-  if (B == 0) return FP_OK;
-  if (chunk <= 0) chunk = 1 << 18;
-  chunk = (chunk + kThreads - 1) / kThreads * kThreads;
-  std::lock_guard<std::mutex> lock(g_pipe.mu);
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return cuda_status(e);
-  // Per slot: inputs then outputs for `chunk` paths, 256-byte aligned pieces.
-  const int64_t w_in[5] = {6 * K, 3 * K, 3, 3, 2 * K};
-  const int64_t w_out[7] = {2 * K, 3 * K, 1, 6 * K, 3 * K, 3, 3};
-  auto al = [](size_t x) { return (x + 255) / 256 * 256; };
-  size_t slot = al(size_t(chunk));  // status
-  for (int i = 0; i < 5; ++i) slot += al(size_t(chunk * w_in[i]) * sizeof(float));
-  for (int i = 0; i < 7; ++i) slot += al(size_t(chunk * w_out[i]) * sizeof(float));
-  if (g_pipe.device != dev || int(g_pipe.bufs.size()) != depth || g_pipe.buf_bytes < slot) {
-    if ((e = g_pipe.setup(dev, depth, slot)) != cudaSuccess) {
-      g_pipe.release();
-      return cuda_status(e);
-    }
-  }
-  const float* hin[5] = {basis, anchor, start, end, T0};
-  float* hout[7] = {T_out, points_out, length_out, d_basis, d_anchor, d_start, d_end};
-  // Chunk schedule: ramp up from chunk/8 (the first copy-out starts after one
-  // small copy-in + solve) and back down at the end (short drain); full
-  // chunks in between.
-  std::vector<int64_t> sizes;
-  {
-    const int64_t r[3] = {chunk / 8, chunk / 4, chunk / 2};
-    std::vector<int64_t> head, tail;
-    int64_t left = B;
-    for (int i = 0; i < 3 && left > 0; ++i) {
-      const int64_t h = std::min<int64_t>((r[i] + kThreads - 1) / kThreads * kThreads, left);
-      head.push_back(h);
-      left -= h;
-      if (left <= 0) break;
-      const int64_t t = std::min<int64_t>((r[i] + kThreads - 1) / kThreads * kThreads, left);
-      tail.push_back(t);
-      left -= t;
-    }
-    sizes = head;
-    for (; left > 0; left -= std::min(left, chunk)) sizes.push_back(std::min(left, chunk));
-    sizes.insert(sizes.end(), tail.rbegin(), tail.rend());
-  }
-  cudaStream_t s_in = g_pipe.s_in, s_k = g_pipe.s_k, s_out = g_pipe.s_out;
-  int64_t c = 0, lo = 0;
-  for (const int64_t n : sizes) {
-    const int j = int(c % depth);
-    char* p = static_cast<char*>(g_pipe.bufs[j]);
-    float* din[5];
-    float* dout[7];
-    for (int i = 0; i < 5; ++i) {
-      din[i] = reinterpret_cast<float*>(p);
-      p += al(size_t(chunk * w_in[i]) * sizeof(float));
-    }
-    for (int i = 0; i < 7; ++i) {
-      dout[i] = reinterpret_cast<float*>(p);
-      p += al(size_t(chunk * w_out[i]) * sizeof(float));
-    }
-    uint8_t* dst = reinterpret_cast<uint8_t*>(p);
-    // copy in (the slot's input region is free once chunk c - depth's kernel ran)
-    if (c >= depth && (e = cudaStreamWaitEvent(s_in, g_pipe.ev_k[j], 0)) != cudaSuccess)
-      return cuda_status(e);
-    {
-      void *dv[5], *sv[5];
-      size_t nb[5], m = 0;
-      for (int i = 0; i < 5; ++i) {
-        if (w_in[i] == 0 || hin[i] == nullptr) continue;
-        dv[m] = din[i];
-        sv[m] = const_cast<float*>(hin[i] + lo * w_in[i]);
-        nb[m++] = size_t(n * w_in[i]) * sizeof(float);
-      }
-      if ((e = copy_arrays(dv, sv, nb, m, cudaMemcpyHostToDevice, s_in)) != cudaSuccess)
-        return cuda_status(e);
-    }
-    if ((e = cudaEventRecord(g_pipe.ev_in[j], s_in)) != cudaSuccess) return cuda_status(e);
-    // solve + VJP (the output region is free once chunk c - depth was copied out)
-    if ((e = cudaStreamWaitEvent(s_k, g_pipe.ev_in[j], 0)) != cudaSuccess) return cuda_status(e);
-    if (c >= depth && (e = cudaStreamWaitEvent(s_k, g_pipe.ev_out[j], 0)) != cudaSuccess)
-      return cuda_status(e);
-    // Tile kernel (no host round trip): the bucketed plan would synchronise
-    // its stream and stall this enqueue loop.
-    int rc = solve_vjp_impl<float>(din[0], din[1], din[2], din[3], din[4], n, K, iterations, fp_iters,
-                                   nullptr, w_L_scale, mode, hout[0] ? dout[0] : nullptr,
-                                   hout[1] ? dout[1] : nullptr, hout[2] ? dout[2] : nullptr,
-                                   hout[3] ? dout[3] : nullptr, hout[4] ? dout[4] : nullptr,
-                                   hout[5] ? dout[5] : nullptr, hout[6] ? dout[6] : nullptr,
-                                   status_out ? dst : nullptr, s_k, kRouteNoSync);
-    if (rc != FP_OK) return rc;
-    if ((e = cudaEventRecord(g_pipe.ev_k[j], s_k)) != cudaSuccess) return cuda_status(e);
-    // copy out
-    if ((e = cudaStreamWaitEvent(s_out, g_pipe.ev_k[j], 0)) != cudaSuccess) return cuda_status(e);
-    {
-      void *dv[8], *sv[8];
-      size_t nb[8], m = 0;
-      for (int i = 0; i < 7; ++i) {
-        if (w_out[i] == 0 || hout[i] == nullptr) continue;
-        dv[m] = hout[i] + lo * w_out[i];
-        sv[m] = dout[i];
-        nb[m++] = size_t(n * w_out[i]) * sizeof(float);
-      }
-      if (status_out) {
-        dv[m] = status_out + lo;
-        sv[m] = dst;
-        nb[m++] = size_t(n);
-      }
-      if ((e = copy_arrays(dv, sv, nb, m, cudaMemcpyDeviceToHost, s_out)) != cudaSuccess)
-        return cuda_status(e);
-    }
-    if ((e = cudaEventRecord(g_pipe.ev_out[j], s_out)) != cudaSuccess) return cuda_status(e);
-    lo += n;
-    ++c;
-  }
-  for (cudaStream_t s : {s_in, s_k, s_out}) {
-    e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) return cuda_status(e);
-  }
-  return FP_OK;
+  return host_pipeline<float>(basis, anchor, start, end, T0, B, K, iterations, fp_iters, w_L_scale,
+                              mode, T_out, points_out, length_out, d_basis, d_anchor, d_start, d_end,
+                              status_out, chunk, depth);
+}
+
+int fp_solve_vjp_host_f64(const double* basis, const double* anchor, const double* start,
+                          const double* end, const double* T0, int64_t B, int K, int iterations,
+                          int fp_iters, double w_L_scale, int mode, double* T_out,
+                          double* points_out, double* length_out, double* d_basis,
+                          double* d_anchor, double* d_start, double* d_end, uint8_t* status_out,
+                          int64_t chunk, int depth) {
+  return host_pipeline<double>(basis, anchor, start, end, T0, B, K, iterations, fp_iters, w_L_scale,
+                               mode, T_out, points_out, length_out, d_basis, d_anchor, d_start,
+                               d_end, status_out, chunk, depth);
 }
 
 int fp_objective_f64(const double* basis, const double* anchor, const double* start,

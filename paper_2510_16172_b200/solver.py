@@ -125,21 +125,17 @@ def solve(scene: BatchScene, T0=None, opts: SolveOptions = SolveOptions(), *,
 
 def solve_with_gradients(scene: BatchScene, T0=None, opts: SolveOptions = SolveOptions(
         precision=Precision.SINGLE), weight=1.0, mode: str = "full"):
-    """Fused forward solve + implicit VJP of sum_b w_b L*_b (one kernel, fp32).
+    """Fused forward solve + implicit VJP of sum_b w_b L*_b (one kernel).
 
-    Returns (SolveResult without g, SceneGradients). `weight` is a scalar or a
-    (B,) tensor of cotangents on the optimal lengths.
+    fp32 or fp64 per `opts.precision`. Returns (SolveResult without g,
+    SceneGradients). `weight` is a scalar or a (B,) tensor of cotangents on
+    the optimal lengths. `mode` is "full" or "envelope".
     """
-    if opts.precision is not Precision.SINGLE:
-        res = solve(scene, T0, opts)
-        from .implicit_diff import vjp_batch
-        grads, st, _ = vjp_batch(scene.astype(opts.precision.dtype), res.T, w_L=weight, mode=mode)
-        res.status = res.status | (st & ~(_lib.STATUS_DEGENERATE_ENTRY | _lib.STATUS_ZERO_DIRECTION))
-        return res, grads
+    single = opts.precision is Precision.SINGLE
     lib = _lib.load()
-    sc = scene.astype(np.float32)
+    sc = scene.astype(opts.precision.dtype)
     B, K = sc.size, sc.n
-    dt, dev = torch.float32, sc.basis.device
+    dt, dev = (torch.float32 if single else torch.float64), sc.basis.device
     T0 = torch.zeros(B, K, 2, dtype=dt, device=dev) if T0 is None else params_tensor(sc, T0)
     wt = None
     scale = 1.0
@@ -151,56 +147,69 @@ def solve_with_gradients(scene: BatchScene, T0=None, opts: SolveOptions = SolveO
                       length=_empty((B,), dt, dev), status=_empty((B,), torch.uint8, dev))
     grads = SceneGradients(_empty((B, K, 3, 2), dt, dev), _empty((B, K, 3), dt, dev),
                            _empty((B, 3), dt, dev), _empty((B, 3), dt, dev))
-    rc = lib.fp_solve_vjp_f32(ptr(sc.basis), ptr(sc.anchor), ptr(sc.start), ptr(sc.end), ptr(T0),
-                              B, K, opts.iterations, opts.fixed_point_iters, ptr(wt), scale,
-                              _MODES[mode], ptr(res.T), ptr(res.points), ptr(res.length),
-                              ptr(grads.basis), ptr(grads.anchor), ptr(grads.start),
-                              ptr(grads.end), ptr(res.status), stream_ptr())
-    _lib.check(rc, "fp_solve_vjp_f32")
+    name = "fp_solve_vjp_f32" if single else "fp_solve_vjp_f64"
+    rc = getattr(lib, name)(ptr(sc.basis), ptr(sc.anchor), ptr(sc.start), ptr(sc.end), ptr(T0),
+                            B, K, opts.iterations, opts.fixed_point_iters, ptr(wt), scale,
+                            _MODES[mode], ptr(res.T), ptr(res.points), ptr(res.length),
+                            ptr(grads.basis), ptr(grads.anchor), ptr(grads.start),
+                            ptr(grads.end), ptr(res.status), stream_ptr())
+    _lib.check(rc, name)
     return res, grads
 
 
 def solve_with_gradients_host(basis, anchor, start, end, T0=None, iterations: int = 20,
                               fixed_point_iters: int = 1, weight: float = 1.0, mode: str = "full",
-                              chunk: int = 1 << 19, depth: int = 3, out=None):
-    """solve_with_gradients for host (numpy) arrays in the reference layout, fp32.
+                              chunk: int = 1 << 19, depth: int = 3, out=None,
+                              precision: Precision | None = None):
+    """solve_with_gradients for host (numpy) arrays in the reference layout.
 
-    One call of fp_solve_vjp_host_f32: the batch streams through the GPU in
-    chunks (copy-in, compute and copy-out streams over a ring of `depth`
-    device chunk slots), so both PCIe directions and compute overlap. Pinned (page-locked) arrays transfer fastest:
-    pass `out` from `host_buffers` to reuse pinned outputs. Returns a dict of
-    numpy arrays: T, points, length, status, d_basis, d_anchor, d_start, d_end.
+    One call of fp_solve_vjp_host_f32 / _f64: the batch streams through the
+    GPU in chunks (copy-in, compute and copy-out streams over a ring of
+    `depth` device chunk slots), so both PCIe directions and compute overlap.
+    `precision` defaults to the dtype of `basis` (float64 arrays run the fp64
+    kernels, never a silent fp32 downcast). Pinned (page-locked) arrays
+    transfer fastest: pass `out` from `host_buffers` to reuse pinned outputs.
+    Returns a dict of numpy arrays: T, points, length, status, d_basis,
+    d_anchor, d_start, d_end.
     """
     lib = _lib.load()
-    f32 = np.float32
-    basis = np.ascontiguousarray(basis, f32)
+    if precision is None:
+        precision = Precision.DOUBLE if np.asarray(basis).dtype == np.float64 else Precision.SINGLE
+    ft = precision.dtype
+    basis = np.ascontiguousarray(basis, ft)
     B, K = basis.shape[0], basis.shape[1]
-    anchor = np.ascontiguousarray(anchor, f32)
-    start = np.ascontiguousarray(start, f32)
-    end = np.ascontiguousarray(end, f32)
-    T0 = np.zeros((B, K, 2), f32) if T0 is None else np.ascontiguousarray(T0, f32)
+    anchor = np.ascontiguousarray(anchor, ft)
+    start = np.ascontiguousarray(start, ft)
+    end = np.ascontiguousarray(end, ft)
+    T0 = np.zeros((B, K, 2), ft) if T0 is None else np.ascontiguousarray(T0, ft)
     if anchor.shape != (B, K, 3) or start.shape != (B, 3) or end.shape != (B, 3) or T0.shape != (B, K, 2):
         raise ShapeMismatch("host arrays must be basis (B,K,3,2), anchor (B,K,3), start/end (B,3), T0 (B,K,2)")
     if iterations < 1 or fixed_point_iters < 1:
         raise ValueError("iterations and fixed_point_iters must be >= 1")
-    out = out if out is not None else host_buffers(B, K, pinned=False)
+    out = out if out is not None else host_buffers(B, K, pinned=False, precision=precision)
+    for k, v in out.items():
+        want = np.uint8 if k == "status" else ft
+        if v.dtype != want or not v.flags.c_contiguous:
+            raise ShapeMismatch(f"out[{k!r}] must be a C-contiguous {np.dtype(want).name} array")
     P = lambda a: a.ctypes.data  # noqa: E731
-    rc = lib.fp_solve_vjp_host_f32(P(basis), P(anchor), P(start), P(end), P(T0), B, K, iterations,
-                                   fixed_point_iters, float(weight), _MODES[mode], P(out["T"]),
-                                   P(out["points"]), P(out["length"]), P(out["d_basis"]),
-                                   P(out["d_anchor"]), P(out["d_start"]), P(out["d_end"]),
-                                   P(out["status"]), int(chunk), int(depth))
-    _lib.check(rc, "fp_solve_vjp_host_f32")
+    name = "fp_solve_vjp_host_f32" if precision is Precision.SINGLE else "fp_solve_vjp_host_f64"
+    rc = getattr(lib, name)(P(basis), P(anchor), P(start), P(end), P(T0), B, K, iterations,
+                            fixed_point_iters, float(weight), _MODES[mode], P(out["T"]),
+                            P(out["points"]), P(out["length"]), P(out["d_basis"]),
+                            P(out["d_anchor"]), P(out["d_start"]), P(out["d_end"]),
+                            P(out["status"]), int(chunk), int(depth))
+    _lib.check(rc, name)
     return out
 
 
-def host_buffers(B: int, K: int, pinned: bool = True) -> dict:
+def host_buffers(B: int, K: int, pinned: bool = True, precision: Precision = Precision.SINGLE) -> dict:
     """Output arrays for solve_with_gradients_host (page-locked when pinned)."""
     def mk(shape, dt):
         if pinned:
             return torch.empty(shape, dtype=dt, pin_memory=True).numpy()
         return np.empty(shape, dtype=torch.empty(0, dtype=dt).numpy().dtype)
-    f, u8 = torch.float32, torch.uint8
+    f = torch.float32 if precision is Precision.SINGLE else torch.float64
+    u8 = torch.uint8
     return {"T": mk((B, K, 2), f), "points": mk((B, K, 3), f), "length": mk((B,), f),
             "status": mk((B,), u8), "d_basis": mk((B, K, 3, 2), f), "d_anchor": mk((B, K, 3), f),
             "d_start": mk((B, 3), f), "d_end": mk((B, 3), f)}

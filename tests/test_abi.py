@@ -43,3 +43,25 @@ def test_sass_is_sm100a():
         pytest.skip("cuobjdump not available")
     out = subprocess.run([cuobjdump, "--list-elf", _lib.LIB_PATH], capture_output=True, text=True)
     assert "sm_100a" in out.stdout
+
+
+def test_host_entry_precision_follows_the_arrays():
+    """solve_with_gradients_host never downcasts float64 arrays: DOUBLE is
+    inferred, fp64 output buffers are required (checked before any CUDA call)."""
+    from paper_2510_16172_b200 import ShapeMismatch
+    from paper_2510_16172_b200.solver import Precision, host_buffers, solve_with_gradients_host
+
+    B, K = 4, 2
+    out64 = host_buffers(B, K, pinned=False, precision=Precision.DOUBLE)
+    assert out64["d_basis"].dtype == np.float64 and out64["status"].dtype == np.uint8
+    assert host_buffers(B, K, pinned=False)["T"].dtype == np.float32
+    f8 = np.zeros
+    args = (f8((B, K, 3, 2)), f8((B, K, 3)), f8((B, 3)), f8((B, 3)))
+    with pytest.raises(ShapeMismatch):  # float64 inputs with fp32 outputs
+        solve_with_gradients_host(*args, out=host_buffers(B, K, pinned=False))
+    lib = _lib.load()
+    null = None
+    for fn in (lib.fp_solve_vjp_host_f32, lib.fp_solve_vjp_host_f64):
+        assert fn(*([null] * 5), -1, K, 20, 1, 1.0, 0, *([null] * 8), 0, 3) == 1
+        assert fn(*([null] * 5), B, K, 20, 1, 1.0, 0, *([null] * 8), 0, 9) == 1  # depth > 8
+        assert fn(*([null] * 5), 0, K, 20, 1, 1.0, 0, *([null] * 8), 0, 3) == 0  # empty batch

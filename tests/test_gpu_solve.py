@@ -118,11 +118,13 @@ def test_known_answers():
         fp.line_search_alpha(spec, np.array([[0.0, 2.0]]), np.zeros((1, 2)))
 
 
-def test_batch_invariance_bitwise():
-    """Results per path do not depend on batch size, order or alignment."""
+@pytest.mark.parametrize("prec", [Precision.SINGLE, Precision.DOUBLE])
+def test_batch_invariance_bitwise(prec):
+    """Results per path do not depend on batch size, order or alignment,
+    in fp32 and in fp64 (a permuted batch is a scattered layout: bucketed dispatch)."""
     b = datagen.gen_batch(7, datagen.all_orderings(3), 300)  # 2400 rows: ragged last CTA
     sc = BatchScene(b.basis, b.anchor, b.start, b.end)
-    opts = SolveOptions(iterations=20, precision=Precision.SINGLE)
+    opts = SolveOptions(iterations=20, precision=prec)
     full = solve(sc, b.T0, opts)
     perm = np.random.default_rng(0).permutation(b.size)
     scp = BatchScene(b.basis[perm], b.anchor[perm], b.start[perm], b.end[perm])
@@ -254,18 +256,21 @@ def test_specialised_kernels_match_dense(K):
 
 @pytest.mark.parametrize("K", [1, 2, 3, 4, 5])
 @pytest.mark.parametrize("layout", ["ordered", "interleaved"])
-def test_tile_and_bucketed_dispatch_bitwise_equal(K, layout):
+@pytest.mark.parametrize("prec", ["single", "double"])
+def test_tile_and_bucketed_dispatch_bitwise_equal(K, layout, prec):
     """Every non-dense policy runs each path through its own kind-mask variant:
     the tile kernel (per-warp dispatch, mixed warps diverge) and the bucketed
-    per-mask kernels give the same bits, for ordering-major and scattered
-    layouts (include/fermat_b200.h, FP_POLICY_*)."""
+    path (fp32: per-mask kernels; fp64: the tile kernel over a mask-sorted
+    permutation) give the same bits, for ordering-major and scattered layouts
+    (include/fermat_b200.h, FP_POLICY_*), so results never depend on the
+    policy's layout history."""
     from paper_2510_16172_b200.solver import solve_with_gradients
 
     b = datagen.gen_batch(40 + K, datagen.all_orderings(K), 300)
     if layout == "interleaved":
         b = datagen.interleave(b, seed=K)
     sc = BatchScene(b.basis, b.anchor, b.start, b.end)
-    opts = SolveOptions(iterations=20, precision=Precision.SINGLE)
+    opts = SolveOptions(iterations=20, precision=Precision.SINGLE if prec == "single" else Precision.DOUBLE)
     out = {}
     try:
         for pol in ("tile", "bucket", "serial", "auto"):

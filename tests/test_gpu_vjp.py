@@ -160,3 +160,42 @@ def test_host_pipeline_equals_device_step(K, chunk):
                           ("status", res.status), ("d_basis", grads.basis), ("d_anchor", grads.anchor),
                           ("d_start", grads.start), ("d_end", grads.end)):
             assert np.array_equal(out[name], dev.cpu().numpy()), (name, pinned, depth)
+
+
+def test_fused_step_fp64_equals_solve_then_vjp_bitwise():
+    """Precision.DOUBLE (the reference default, solver.py:46) runs the fused fp64
+    kernel; it returns the bits of the fp64 solve followed by the fp64 VJP."""
+    b = datagen.gen_batch(12, datagen.all_orderings(3), 96)
+    sc = BatchScene(b.basis, b.anchor, b.start, b.end)
+    opts = SolveOptions(iterations=20, precision=Precision.DOUBLE)
+    res, grads = solve_with_gradients(sc, b.T0, opts, weight=1.0, mode="full")
+    assert res.T.dtype == torch.float64 and grads.basis.dtype == torch.float64
+    sep = solve(sc, b.T0, opts)
+    g2, st2, _ = vjp_batch(sc.astype(np.float64), sep.T, w_L=1.0, mode="full")
+    assert torch.equal(res.T, sep.T)
+    assert torch.equal(res.length, sep.length)
+    for a, c in ((grads.basis, g2.basis), (grads.anchor, g2.anchor), (grads.start, g2.start),
+                 (grads.end, g2.end)):
+        assert torch.equal(a, c)
+
+
+@pytest.mark.parametrize("K,chunk", [(3, 512), (2, 1 << 19)])
+def test_host_pipeline_fp64_equals_device_step(K, chunk):
+    """float64 host arrays run fp_solve_vjp_host_f64 (no fp32 downcast) and
+    return the fused fp64 device step's bits."""
+    from paper_2510_16172_b200.solver import host_buffers, solve_with_gradients_host
+
+    b = datagen.gen_batch(70 + K, datagen.all_orderings(K), 1300 // 2 ** K + 5)
+    f8 = np.float64
+    sc = BatchScene(b.basis, b.anchor, b.start, b.end)
+    res, grads = solve_with_gradients(sc, b.T0, SolveOptions(iterations=20, precision=Precision.DOUBLE))
+    for pinned in (True, False):
+        out = solve_with_gradients_host(b.basis.astype(f8), b.anchor.astype(f8), b.start.astype(f8),
+                                        b.end.astype(f8), b.T0.astype(f8), iterations=20, chunk=chunk,
+                                        out=host_buffers(b.size, K, pinned=pinned,
+                                                         precision=Precision.DOUBLE))
+        assert out["T"].dtype == np.float64
+        for name, dev in (("T", res.T), ("points", res.points), ("length", res.length),
+                          ("status", res.status), ("d_basis", grads.basis), ("d_anchor", grads.anchor),
+                          ("d_start", grads.start), ("d_end", grads.end)):
+            assert np.array_equal(out[name], dev.cpu().numpy()), (name, pinned)
