@@ -662,79 +662,87 @@ static int host_pipeline(const R* basis, const R* anchor, const R* start, const 
     sizes.insert(sizes.end(), tail.rbegin(), tail.rend());
   }
   cudaStream_t s_in = g_pipe.s_in, s_k = g_pipe.s_k, s_out = g_pipe.s_out;
-  int64_t c = 0, lo = 0;
-  for (const int64_t n : sizes) {
-    const int j = int(c % depth);
-    char* p = static_cast<char*>(g_pipe.bufs[j]);
-    R* din[5];
-    R* dout[7];
-    for (int i = 0; i < 5; ++i) {
-      din[i] = reinterpret_cast<R*>(p);
-      p += al(size_t(chunk * w_in[i]) * sizeof(R));
-    }
-    for (int i = 0; i < 7; ++i) {
-      dout[i] = reinterpret_cast<R*>(p);
-      p += al(size_t(chunk * w_out[i]) * sizeof(R));
-    }
-    uint8_t* dst = reinterpret_cast<uint8_t*>(p);
-    // copy in (the slot's input region is free once chunk c - depth's kernel ran)
-    if (c >= depth && (e = cudaStreamWaitEvent(s_in, g_pipe.ev_k[j], 0)) != cudaSuccess)
-      return cuda_status(e);
-    {
-      void *dv[5], *sv[5];
-      size_t nb[5], m = 0;
+  // Enqueue every chunk; on an error stop enqueuing but still drain the
+  // streams below, so no copy or kernel of this call is in flight when the
+  // next call reuses (or reallocates) the slots.
+  auto enqueue = [&]() -> int {
+    cudaError_t e;
+    int64_t c = 0, lo = 0;
+    for (const int64_t n : sizes) {
+      const int j = int(c % depth);
+      char* p = static_cast<char*>(g_pipe.bufs[j]);
+      R* din[5];
+      R* dout[7];
       for (int i = 0; i < 5; ++i) {
-        if (w_in[i] == 0 || hin[i] == nullptr) continue;
-        dv[m] = din[i];
-        sv[m] = const_cast<R*>(hin[i] + lo * w_in[i]);
-        nb[m++] = size_t(n * w_in[i]) * sizeof(R);
+        din[i] = reinterpret_cast<R*>(p);
+        p += al(size_t(chunk * w_in[i]) * sizeof(R));
       }
-      if ((e = copy_arrays(dv, sv, nb, m, cudaMemcpyHostToDevice, s_in)) != cudaSuccess)
-        return cuda_status(e);
-    }
-    if ((e = cudaEventRecord(g_pipe.ev_in[j], s_in)) != cudaSuccess) return cuda_status(e);
-    // solve + VJP (the output region is free once chunk c - depth was copied out)
-    if ((e = cudaStreamWaitEvent(s_k, g_pipe.ev_in[j], 0)) != cudaSuccess) return cuda_status(e);
-    if (c >= depth && (e = cudaStreamWaitEvent(s_k, g_pipe.ev_out[j], 0)) != cudaSuccess)
-      return cuda_status(e);
-    // Tile kernel (no host round trip): the bucketed plan would synchronise
-    // its stream and stall this enqueue loop.
-    int rc = solve_vjp_impl<R>(din[0], din[1], din[2], din[3], din[4], n, K, iterations, fp_iters,
-                                   nullptr, w_L_scale, mode, hout[0] ? dout[0] : nullptr,
-                                   hout[1] ? dout[1] : nullptr, hout[2] ? dout[2] : nullptr,
-                                   hout[3] ? dout[3] : nullptr, hout[4] ? dout[4] : nullptr,
-                                   hout[5] ? dout[5] : nullptr, hout[6] ? dout[6] : nullptr,
-                                   status_out ? dst : nullptr, s_k, kRouteNoSync);
-    if (rc != FP_OK) return rc;
-    if ((e = cudaEventRecord(g_pipe.ev_k[j], s_k)) != cudaSuccess) return cuda_status(e);
-    // copy out
-    if ((e = cudaStreamWaitEvent(s_out, g_pipe.ev_k[j], 0)) != cudaSuccess) return cuda_status(e);
-    {
-      void *dv[8], *sv[8];
-      size_t nb[8], m = 0;
       for (int i = 0; i < 7; ++i) {
-        if (w_out[i] == 0 || hout[i] == nullptr) continue;
-        dv[m] = hout[i] + lo * w_out[i];
-        sv[m] = dout[i];
-        nb[m++] = size_t(n * w_out[i]) * sizeof(R);
+        dout[i] = reinterpret_cast<R*>(p);
+        p += al(size_t(chunk * w_out[i]) * sizeof(R));
       }
-      if (status_out) {
-        dv[m] = status_out + lo;
-        sv[m] = dst;
-        nb[m++] = size_t(n);
-      }
-      if ((e = copy_arrays(dv, sv, nb, m, cudaMemcpyDeviceToHost, s_out)) != cudaSuccess)
+      uint8_t* dst = reinterpret_cast<uint8_t*>(p);
+      // copy in (the slot's input region is free once chunk c - depth's kernel ran)
+      if (c >= depth && (e = cudaStreamWaitEvent(s_in, g_pipe.ev_k[j], 0)) != cudaSuccess)
         return cuda_status(e);
+      {
+        void *dv[5], *sv[5];
+        size_t nb[5], m = 0;
+        for (int i = 0; i < 5; ++i) {
+          if (w_in[i] == 0 || hin[i] == nullptr) continue;
+          dv[m] = din[i];
+          sv[m] = const_cast<R*>(hin[i] + lo * w_in[i]);
+          nb[m++] = size_t(n * w_in[i]) * sizeof(R);
+        }
+        if ((e = copy_arrays(dv, sv, nb, m, cudaMemcpyHostToDevice, s_in)) != cudaSuccess)
+          return cuda_status(e);
+      }
+      if ((e = cudaEventRecord(g_pipe.ev_in[j], s_in)) != cudaSuccess) return cuda_status(e);
+      // solve + VJP (the output region is free once chunk c - depth was copied out)
+      if ((e = cudaStreamWaitEvent(s_k, g_pipe.ev_in[j], 0)) != cudaSuccess) return cuda_status(e);
+      if (c >= depth && (e = cudaStreamWaitEvent(s_k, g_pipe.ev_out[j], 0)) != cudaSuccess)
+        return cuda_status(e);
+      // Tile kernel (no host round trip): the bucketed plan would synchronise
+      // its stream and stall this enqueue loop.
+      int rc = solve_vjp_impl<R>(din[0], din[1], din[2], din[3], din[4], n, K, iterations, fp_iters,
+                                     nullptr, w_L_scale, mode, hout[0] ? dout[0] : nullptr,
+                                     hout[1] ? dout[1] : nullptr, hout[2] ? dout[2] : nullptr,
+                                     hout[3] ? dout[3] : nullptr, hout[4] ? dout[4] : nullptr,
+                                     hout[5] ? dout[5] : nullptr, hout[6] ? dout[6] : nullptr,
+                                     status_out ? dst : nullptr, s_k, kRouteNoSync);
+      if (rc != FP_OK) return rc;
+      if ((e = cudaEventRecord(g_pipe.ev_k[j], s_k)) != cudaSuccess) return cuda_status(e);
+      // copy out
+      if ((e = cudaStreamWaitEvent(s_out, g_pipe.ev_k[j], 0)) != cudaSuccess) return cuda_status(e);
+      {
+        void *dv[8], *sv[8];
+        size_t nb[8], m = 0;
+        for (int i = 0; i < 7; ++i) {
+          if (w_out[i] == 0 || hout[i] == nullptr) continue;
+          dv[m] = hout[i] + lo * w_out[i];
+          sv[m] = dout[i];
+          nb[m++] = size_t(n * w_out[i]) * sizeof(R);
+        }
+        if (status_out) {
+          dv[m] = status_out + lo;
+          sv[m] = dst;
+          nb[m++] = size_t(n);
+        }
+        if ((e = copy_arrays(dv, sv, nb, m, cudaMemcpyDeviceToHost, s_out)) != cudaSuccess)
+          return cuda_status(e);
+      }
+      if ((e = cudaEventRecord(g_pipe.ev_out[j], s_out)) != cudaSuccess) return cuda_status(e);
+      lo += n;
+      ++c;
     }
-    if ((e = cudaEventRecord(g_pipe.ev_out[j], s_out)) != cudaSuccess) return cuda_status(e);
-    lo += n;
-    ++c;
-  }
+    return FP_OK;
+  };
+  int rc = enqueue();
   for (cudaStream_t s : {s_in, s_k, s_out}) {
-    e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) return cuda_status(e);
+    const cudaError_t se = cudaStreamSynchronize(s);
+    if (se != cudaSuccess && rc == FP_OK) rc = cuda_status(se);
   }
-  return FP_OK;
+  return rc;
 }
 
 }  // namespace fp

@@ -72,6 +72,11 @@ __global__ void __launch_bounds__(kThreads, (MinBlocks<float, Lay<K, MASK>::NA>:
   constexpr int NA = L::NA;
   const int lane = threadIdx.x & 31;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  // candidates / converged / in-bounds: per-CTA shared counters, one global
+  // atomic each per CTA (not per warp: 8M warps on three addresses)
+  __shared__ unsigned int cta_count[3];
+  if (threadIdx.x < 3) cta_count[threadIdx.x] = 0;
+  __syncthreads();
   for (int64_t c0 = a.cand_begin + int64_t(blockIdx.x) * blockDim.x; c0 < a.cand_end; c0 += stride) {
     const int64_t c = c0 + threadIdx.x;
     const bool live = c < a.cand_end;
@@ -118,9 +123,9 @@ __global__ void __launch_bounds__(kThreads, (MinBlocks<float, Lay<K, MASK>::NA>:
                    bi = __ballot_sync(0xffffffffu, live && inb), bv = __ballot_sync(0xffffffffu, valid);
     unsigned long long base = 0;
     if (lane == 0) {
-      atomicAdd(&a.counters[0], (unsigned long long)__popc(bl));
-      if (bc) atomicAdd(&a.counters[1], (unsigned long long)__popc(bc));
-      if (bi) atomicAdd(&a.counters[2], (unsigned long long)__popc(bi));
+      atomicAdd_block(&cta_count[0], unsigned(__popc(bl)));
+      if (bc) atomicAdd_block(&cta_count[1], unsigned(__popc(bc)));
+      if (bi) atomicAdd_block(&cta_count[2], unsigned(__popc(bi)));
       if (bv) base = atomicAdd(&a.counters[3], (unsigned long long)__popc(bv));
     }
     base = __shfl_sync(0xffffffffu, base, 0);
@@ -198,6 +203,9 @@ __global__ void __launch_bounds__(kThreads, (MinBlocks<float, Lay<K, MASK>::NA>:
       }
     }
   }
+  __syncthreads();
+  if (threadIdx.x < 3 && cta_count[threadIdx.x])
+    atomicAdd(&a.counters[threadIdx.x], (unsigned long long)cta_count[threadIdx.x]);
 }
 
 // Decode-only kernel (enumeration parity tests, `enumerate_candidates`).
