@@ -167,18 +167,20 @@ int fp_enum_decode(const int32_t* plane_ids, int n_planes, const int32_t* edge_i
  * accumulated): candidates, converged, in-bounds, valid (= records written
  * when below `capacity`). With obj_grad (N,9: basis 6 + anchor 3) non-NULL,
  * also accumulates loss += sum 1/L^2 and the gradients of that loss (full
- * implicit VJP, cotangent -2/L^3) into obj_grad, tx_grad (3), rx_grad (n_rx,3). */
+ * implicit VJP, cotangent -2/L^3) into obj_grad, tx_grad (3), rx_grad (n_rx,3)
+ * and loss — fp64 accumulators (each path's terms are fp32). */
 int fp_enum_trace_f32(const float* obj_basis, const float* obj_anchor, const int32_t* plane_ids,
                       int n_planes, const int32_t* edge_ids, int n_edges, const float* tx,
                       const float* rx, int n_rx, int order, unsigned pattern, int64_t cand_begin,
                       int64_t cand_end, int iterations, int fp_iters,
                       unsigned long long* counters, int64_t capacity, int32_t* rec_rx,
                       int32_t* rec_seq, float* rec_T, float* rec_L, float* rec_points,
-                      float* obj_grad, float* tx_grad, float* rx_grad, float* loss, void* stream);
+                      double* obj_grad, double* tx_grad, double* rx_grad, double* loss,
+                      void* stream);
 /* Object-parameter gradients -> vertex gradients: vert_ids (N,4) (-1 unused),
  * coef (N,3,4) for (anchor, basis col 0, basis col 1) x vertex slot. */
-int fp_vertex_chain_f32(const float* obj_grad, int n_objects, const int32_t* vert_ids,
-                        const float* coef, float* vertex_grad, void* stream);
+int fp_vertex_chain_f32(const double* obj_grad, int n_objects, const int32_t* vert_ids,
+                        const float* coef, double* vertex_grad, void* stream);
 
 /* ---- visibility of traced paths (post-processing; no reference code) --------
  * For n traced paths of order 1..3 (TX, interaction points (n, order, 3), RX =

@@ -45,7 +45,7 @@ struct EnumArgs {
   int64_t capacity;
   int32_t *rec_rx, *rec_seq;
   float *rec_T, *rec_L, *rec_points;
-  float *obj_grad, *tx_grad, *rx_grad, *loss;
+  double *obj_grad, *tx_grad, *rx_grad, *loss;  // fp64 accumulators (config 4)
 };
 
 template <int K, unsigned MASK>
@@ -75,6 +75,8 @@ __global__ void __launch_bounds__(kThreads, (MinBlocks<float, Lay<K, MASK>::NA>:
   // candidates / converged / in-bounds: per-CTA shared counters, one global
   // atomic each per CTA (not per warp: 8M warps on three addresses)
   __shared__ unsigned int cta_count[3];
+  // config 4: per-warp staging of each lane's object gradients ([i][lane][9])
+  __shared__ float gstage[GRAD ? kThreads / 32 : 1][GRAD ? K * 32 * 9 : 1];
   if (threadIdx.x < 3) cta_count[threadIdx.x] = 0;
   __syncthreads();
   for (int64_t c0 = a.cand_begin + int64_t(blockIdx.x) * blockDim.x; c0 < a.cand_end; c0 += stride) {
@@ -154,11 +156,17 @@ __global__ void __launch_bounds__(kThreads, (MinBlocks<float, Lay<K, MASK>::NA>:
     }
     if (GRAD) {
       // ---- config 4: loss sum 1/L^2, cotangent -2/L^3, full implicit VJP ----
+      // Per-path terms are fp32 (the solve's precision) and so are the sums
+      // over one warp (<= 32 terms); the global sums over up to ~1e8 valid
+      // paths accumulate in fp64 (fp32 atomics drift by ~1e-3 relative at
+      // that count).
       float lossv = 0.f, g0[3] = {0.f, 0.f, 0.f};
+      bool contrib = false;
+      float* wg = gstage[threadIdx.x >> 5];
       if (valid) {
         const float il = 1.f / len;
-        lossv = il * il;
-        wl = -2.f * lossv * il;
+        const float l2 = il * il;
+        wl = -2.f * l2 * il;
         float tf[K][2], vf[K][2];
 #pragma unroll
         for (int i = 0; i < K; ++i) {
@@ -169,26 +177,65 @@ __global__ void __launch_bounds__(kThreads, (MinBlocks<float, Lay<K, MASK>::NA>:
         SceneGrad<float, K> sg;
         const uint8_t vs = implicit_vjp<float, K, MASK>(G, P, tf, vf, wl, true, true, false, sg);
         if ((vs & FP_STATUS_SINGULAR) == 0) {
+          contrib = true;
+          lossv = l2;
+          // park this path's (basis 6, anchor 3) gradients per interaction in
+          // shared memory ([i][lane][9]) so its registers die here
 #pragma unroll
-          for (int i = 0; i < K; ++i) {
-            float* og = a.obj_grad + int64_t(obj[i]) * 9;
+          for (int i = 0; i < K; ++i)
 #pragma unroll
             for (int r = 0; r < 3; ++r) {
-              atomicAdd(og + 2 * r, sg.db[i][r][0]);
-              if (L::plane(i)) atomicAdd(og + 2 * r + 1, sg.db[i][r][1]);
-              atomicAdd(og + 6 + r, sg.da[i][r]);
+              wg[(i * 32 + lane) * 9 + 2 * r] = sg.db[i][r][0];
+              wg[(i * 32 + lane) * 9 + 2 * r + 1] = sg.db[i][r][1];
+              wg[(i * 32 + lane) * 9 + 6 + r] = sg.da[i][r];
             }
-          }
 #pragma unroll
           for (int r = 0; r < 3; ++r) {
             g0[r] = sg.d0[r];
-            if (a.rx_grad) atomicAdd(a.rx_grad + 3 * rx + r, sg.d1[r]);
+            if (a.rx_grad) atomicAdd(a.rx_grad + 3 * rx + r, double(sg.d1[r]));
           }
-        } else {
-          lossv = 0.f;
         }
       }
-      if (__any_sync(0xffffffffu, valid)) {
+      const unsigned cm = __ballot_sync(0xffffffffu, contrib);
+      if (cm) {
+        // Candidates of a warp are consecutive sequences: they share their
+        // leading objects (the last digit varies fastest). For interactions
+        // 0 .. K-2 the lanes that hit the same object are summed from the
+        // staged gradients (lanes 0..8 each take one element, in lane order)
+        // and added with one atomic per element; the last interaction,
+        // spread over many objects, adds per lane. (Per-lane atomics on the
+        // shared leading objects cost 7% of the config-4 step on the
+        // 192-object alphabet.)
+        __syncwarp();
+        const bool live_e = lane < 9;
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+          // element `lane` of interaction i is inert for edges' second column
+          const bool elem_ok = live_e && (lane >= 6 || (lane & 1) == 0 || L::plane(i));
+          if (i == K - 1) {
+            if (contrib) {
+              double* og = a.obj_grad + int64_t(obj[i]) * 9;
+#pragma unroll
+              for (int e = 0; e < 9; ++e)
+                if (e >= 6 || (e & 1) == 0 || L::plane(i))
+                  atomicAdd(og + e, double(wg[(i * 32 + lane) * 9 + e]));
+            }
+            continue;
+          }
+          unsigned pending = cm;
+          while (pending) {
+            const int leader = __ffs(pending) - 1;
+            const int o = __shfl_sync(0xffffffffu, obj[i], leader);
+            const unsigned grp = __ballot_sync(0xffffffffu, ((pending >> lane) & 1u) && obj[i] == o);
+            pending &= ~grp;
+            if (elem_ok) {
+              float v = 0.f;
+              for (unsigned m = grp; m; m &= m - 1) v += wg[(i * 32 + __ffs(m) - 1) * 9 + lane];
+              atomicAdd(a.obj_grad + int64_t(o) * 9 + lane, double(v));
+            }
+          }
+        }
+        __syncwarp();
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
           lossv += __shfl_xor_sync(0xffffffffu, lossv, off);
@@ -196,9 +243,9 @@ __global__ void __launch_bounds__(kThreads, (MinBlocks<float, Lay<K, MASK>::NA>:
           for (int r = 0; r < 3; ++r) g0[r] += __shfl_xor_sync(0xffffffffu, g0[r], off);
         }
         if (lane == 0) {
-          atomicAdd(a.loss, lossv);
+          atomicAdd(a.loss, double(lossv));
 #pragma unroll
-          for (int r = 0; r < 3; ++r) atomicAdd(a.tx_grad + r, g0[r]);
+          for (int r = 0; r < 3; ++r) atomicAdd(a.tx_grad + r, double(g0[r]));
         }
       }
     }
@@ -305,13 +352,13 @@ static int fill_args(EnumArgs& a, const float* obj_basis, const float* obj_ancho
 // Chain rule from object parameters to wall-vertex coordinates (config 4):
 // every object parameter block (anchor, basis column 0, basis column 1) is a
 // linear combination of at most four vertices, coef (N, 3, 4) x vert_ids (N, 4).
-__global__ void vertex_chain_kernel(const float* __restrict__ obj_grad, int n_objects,
+__global__ void vertex_chain_kernel(const double* __restrict__ obj_grad, int n_objects,
                                     const int32_t* __restrict__ vert_ids, const float* __restrict__ coef,
-                                    float* __restrict__ vertex_grad) {
+                                    double* __restrict__ vertex_grad) {
   const int o = blockIdx.x * blockDim.x + threadIdx.x;
   if (o >= n_objects) return;
-  const float* g = obj_grad + 9 * o;
-  float dp[3][3];
+  const double* g = obj_grad + 9 * o;
+  double dp[3][3];
   for (int r = 0; r < 3; ++r) {
     dp[0][r] = g[6 + r];      // anchor
     dp[1][r] = g[2 * r];      // basis column 0
@@ -321,8 +368,8 @@ __global__ void vertex_chain_kernel(const float* __restrict__ obj_grad, int n_ob
     const int vid = vert_ids[4 * o + v];
     if (vid < 0) continue;
     for (int r = 0; r < 3; ++r) {
-      float acc = 0.f;
-      for (int p = 0; p < 3; ++p) acc = fmaf(coef[12 * o + 4 * p + v], dp[p][r], acc);
+      double acc = 0.0;
+      for (int p = 0; p < 3; ++p) acc = fma(double(coef[12 * o + 4 * p + v]), dp[p][r], acc);
       atomicAdd(vertex_grad + 3 * vid + r, acc);
     }
   }
@@ -363,7 +410,7 @@ int fp_enum_trace_f32(const float* obj_basis, const float* obj_anchor, const int
                       int64_t cand_end, int iterations, int fp_iters,
                       unsigned long long* counters, int64_t capacity, int32_t* rec_rx,
                       int32_t* rec_seq, float* rec_T, float* rec_L, float* rec_points,
-                      float* obj_grad, float* tx_grad, float* rx_grad, float* loss, void* stream) {
+                      double* obj_grad, double* tx_grad, double* rx_grad, double* loss, void* stream) {
   EnumArgs a;
   int rc = fill_args(a, obj_basis, obj_anchor, plane_ids, n_planes, edge_ids, n_edges, tx, rx, n_rx,
                      order, pattern, cand_begin, cand_end);
@@ -395,8 +442,8 @@ int fp_enum_trace_f32(const float* obj_basis, const float* obj_anchor, const int
   return e == cudaSuccess ? FP_OK : FP_ERR_CUDA;
 }
 
-int fp_vertex_chain_f32(const float* obj_grad, int n_objects, const int32_t* vert_ids,
-                        const float* coef, float* vertex_grad, void* stream) {
+int fp_vertex_chain_f32(const double* obj_grad, int n_objects, const int32_t* vert_ids,
+                        const float* coef, double* vertex_grad, void* stream) {
   if (n_objects < 0 || (n_objects > 0 && (!obj_grad || !vert_ids || !coef || !vertex_grad)))
     return FP_ERR_INVALID_ARGUMENT;
   if (n_objects == 0) return FP_OK;

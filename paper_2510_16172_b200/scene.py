@@ -323,9 +323,10 @@ def trace(scene: UrbanScene, max_order: int = 3, iterations: int = 20, fp_iters:
     s = stream_ptr()
     grads = None
     if with_grad:
-        grads = dict(obj=torch.zeros(N, 9, dtype=torch.float32, device=dev),
-                     tx=torch.zeros(3, dtype=torch.float32, device=dev),
-                     loss=torch.zeros(1, dtype=torch.float32, device=dev))
+        # fp64 accumulators: per-path terms are fp32, their sums are not
+        grads = dict(obj=torch.zeros(N, 9, dtype=torch.float64, device=dev),
+                     tx=torch.zeros(3, dtype=torch.float64, device=dev),
+                     loss=torch.zeros(1, dtype=torch.float64, device=dev))
     P = lambda t: None if t is None else t.data_ptr()  # noqa: E731
     counters = torch.zeros(max_order, 4, dtype=torch.int64, device=dev)
     recs = []
@@ -353,7 +354,7 @@ def trace(scene: UrbanScene, max_order: int = 3, iterations: int = 20, fp_iters:
                 P(grads["loss"]) if grads else None, s)
             _lib.check(rc, "fp_enum_trace_f32")
     if with_grad:
-        vg = torch.zeros(scene.walls.shape[0] * 4, 3, dtype=torch.float32, device=dev)
+        vg = torch.zeros(scene.walls.shape[0] * 4, 3, dtype=torch.float64, device=dev)
         rc = lib.fp_vertex_chain_f32(P(grads["obj"]), N, P(ds.vert_ids), P(ds.coef), P(vg), s)
         _lib.check(rc, "fp_vertex_chain_f32")
         if allreduce:
