@@ -244,9 +244,9 @@ int fp_gate_wait(const int* host_flag, double timeout_s, void* stream);
  *   FP_POLICY_AUTO (default): the tile kernel (one launch; each warp
  *     dispatches on its paths' masks; no host round trip; fp32 and fp64)
  *     unless the last call of that order saw more than 1/8 mixed-mask warps
- *     (a scattered layout), which then goes to the bucketed path (fp32: one
- *     kernel per mask; fp64: the tile kernel over a mask-sorted row
- *     permutation).
+ *     (a scattered layout), which then classifies the paths on the device
+ *     (one host round trip) and runs the tile kernel over a mask-sorted row
+ *     permutation.
  *   FP_POLICY_DENSE: the uniform 2K kernel for every path (agrees with the
  *     specialised variants to rounding; used by the tests).
  *   FP_POLICY_AUTO_SERIAL: bucketed, per-mask kernels (fp32) one after

@@ -232,12 +232,13 @@ static int dispatch(int K, const PathArgs<R>& a, int op, cudaStream_t s, int rou
                      (route == kRouteNoSync || tile_preferred(K)));
   if (tile) return cuda_status(run_tile<R>(K, a, op, s));
   if (route == kRouteNoSync || K > kMaxTileOrder) return dispatch_dense_k<R>(K, a, op, s);
-  if constexpr (!is_f32) {
-    // fp64 scattered layout (or a bucketed policy): classify, sort the rows
-    // by kind mask, and run the tile kernel over that permutation, so warps
-    // are uniform and each path still runs its own mask's variant (bitwise
-    // what the tile kernel gives it in any layout; never the dense kernel,
-    // whose rounding differs).
+  if (!is_f32 || (policy == FP_POLICY_AUTO && K <= kAutoTileMaxOrder)) {
+    // Scattered layout under AUTO (and fp64 under every bucketed policy):
+    // classify, sort the rows by kind mask, and run the tile kernel over that
+    // permutation, so warps are uniform and each path still runs its own
+    // mask's variant (bitwise what the tile kernel gives it in any layout;
+    // never the dense kernel, whose rounding differs). One launch, no
+    // per-mask tails.
     BucketScratch sc;
     BucketPlan plan;
     cudaError_t e = bucket_plan<R>(a.basis, B, K, sc, plan, s);
