@@ -381,7 +381,7 @@ def run_ours(args):
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": e_s * 1e3, "raw_paths_per_s": paths_all / e_s,
                "path": "fp_solve_vjp_host_f32 (pinned host buffers; copy-in, compute and copy-out "
-                       "streams over 3 device chunk slots of 2^19 paths)"}
+                       f"streams over 3 device chunk slots of {args.chunk} paths)"}
 
     # ---- CPU baseline (rank 0, N=1 only) ----------------------------------------------
     cpu = None
