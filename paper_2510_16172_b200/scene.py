@@ -297,6 +297,41 @@ def decode_candidates(scene: UrbanScene, order: int, pattern: int, begin: int = 
     return rx, seq
 
 
+def enumerate_candidates(num_objects: int, order: int, *, exclude_repeats: bool = True,
+                         begin: int = 0, end: int | None = None, device=None) -> torch.Tensor:
+    """Every object-index sequence (o_1 .. o_order), o_j in [0, num_objects),
+    in lexicographic order, decoded on the GPU (SURVEY.md §8(b) "enumeration"):
+    int32 (n, order) for the linear candidate range [begin, end).
+
+    exclude_repeats: no immediate repeat (o_j != o_{j+1}; a path cannot
+    interact with the same object twice in a row). The fused tracing kernel
+    (`trace`) decodes the same indices on the fly and never materialises
+    this list. Orders 1..3 (the tracing configs).
+    """
+    if not 1 <= order <= 3:
+        raise ValueError("enumerate_candidates: order must be 1..3")
+    if num_objects < 0:
+        raise ValueError("num_objects must be >= 0")
+    lib = _lib.load()
+    n_obj = int(num_objects)
+    total = n_obj * (n_obj - 1) ** (order - 1) if exclude_repeats else n_obj ** order
+    end = total if end is None else int(end)
+    if not 0 <= begin <= end <= total:
+        raise ValueError(f"candidate range [{begin}, {end}) outside [0, {total})")
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    seq = torch.empty(end - begin, order, dtype=torch.int32, device=dev)
+    if end > begin:
+        ids = torch.arange(n_obj, dtype=torch.int32, device=dev)
+        # One kind everywhere: the decoder skips the previous object at every
+        # position (no immediate repeat). Alternating kinds: consecutive
+        # positions never share a kind, so nothing is skipped (plain product).
+        pattern = (1 << order) - 1 if exclude_repeats else sum(1 << j for j in range(0, order, 2))
+        rc = lib.fp_enum_decode(ids.data_ptr(), n_obj, ids.data_ptr(), n_obj, 1, order, pattern,
+                                begin, end, None, seq.data_ptr(), stream_ptr())
+        _lib.check(rc, "fp_enum_decode")
+    return seq
+
+
 def trace(scene: UrbanScene, max_order: int = 3, iterations: int = 20, fp_iters: int = 1,
           capacity: int | None = None, with_grad: bool = False, points: bool = False,
           rank: int | None = None, world: int | None = None, allreduce: bool = True,

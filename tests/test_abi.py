@@ -65,3 +65,15 @@ def test_host_entry_precision_follows_the_arrays():
         assert fn(*([null] * 5), -1, K, 20, 1, 1.0, 0, *([null] * 8), 0, 3) == 1
         assert fn(*([null] * 5), B, K, 20, 1, 1.0, 0, *([null] * 8), 0, 9) == 1  # depth > 8
         assert fn(*([null] * 5), 0, K, 20, 1, 1.0, 0, *([null] * 8), 0, 3) == 0  # empty batch
+
+
+def test_enumerate_candidates_argument_checks():
+    """Range and order validation happen on the host (no GPU needed)."""
+    from paper_2510_16172_b200 import enumerate_candidates
+
+    with pytest.raises(ValueError):
+        enumerate_candidates(5, 4)
+    with pytest.raises(ValueError):
+        enumerate_candidates(5, 2, begin=0, end=5 * 4 + 1)
+    with pytest.raises(ValueError):
+        enumerate_candidates(5, 2, exclude_repeats=False, begin=3, end=2)

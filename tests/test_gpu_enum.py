@@ -165,3 +165,22 @@ def test_rank_sharding_partitions_every_group():
     for k in range(2):
         for field in ("candidates", "converged", "in_bounds", "valid"):
             assert sum(getattr(p.orders[k], field) for p in parts) == getattr(full.orders[k], field)
+
+
+@pytest.mark.parametrize("order", [1, 2, 3])
+@pytest.mark.parametrize("exclude", [True, False])
+def test_enumerate_candidates_bit_exact(order, exclude):
+    """enumerate_candidates vs itertools: lexicographic, with and
+    without the no-immediate-repeat predicate, whole list and a sub-range."""
+    import itertools
+
+    from paper_2510_16172_b200 import enumerate_candidates
+
+    n = 7
+    ref = np.array([s for s in itertools.product(range(n), repeat=order)
+                    if not exclude or all(a != b for a, b in zip(s, s[1:]))], dtype=np.int32)
+    got = enumerate_candidates(n, order, exclude_repeats=exclude).cpu().numpy()
+    assert np.array_equal(got, ref.reshape(len(ref), order))
+    lo, hi = len(ref) // 3, len(ref) // 3 + 11
+    part = enumerate_candidates(n, order, exclude_repeats=exclude, begin=lo, end=hi).cpu().numpy()
+    assert np.array_equal(part, ref[lo:hi].reshape(hi - lo, order))

@@ -16,6 +16,8 @@ timeout 900 python bench.py --workload config1 --steps 10 > ${O}_bench_cfg1.json
 timeout 900 python bench.py --workload config3 --alphabet walls --visibility --steps 5 > ${O}_bench_cfg3w.json 2>> ${O}_bench.err
 timeout 1200 python bench.py --workload config3 --alphabet all --steps 3 > ${O}_bench_cfg3a.json 2>> ${O}_bench.err
 timeout 900 python bench.py --workload config4 --alphabet walls --steps 5 > ${O}_bench_cfg4w.json 2>> ${O}_bench.err
+timeout 900 python bench.py --workload config4 --alphabet all --steps 2 > ${O}_bench_cfg4a.json 2>> ${O}_bench.err
+timeout 900 python tools/f64_rate.py > ${O}_f64_rate.txt 2>> ${O}_bench.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file ${O}_launches.csv python bench.py --steps 3 --warmup 3 > ${O}_ncu_launch.log 2>&1
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:path_kernel -s 2 -c 1 \
