@@ -466,7 +466,7 @@ def run_scene(args):
 
     def step():
         r = trace(sc, max_order=3, iterations=args.iterations, capacity=cap, with_grad=grad,
-                  device_scene=ds, points=vis)
+                  device_scene=ds, points=vis, gather=args.gather)
         if vis:
             r.vis = [visibility(sc, o, device_scene=ds, blocker_array=blk)[0] for o in r.orders]
         return r
@@ -502,7 +502,10 @@ def run_scene(args):
             "config": {"workload": args.workload, "buildings": 16, "walls": int(sc.walls.shape[0]),
                        "objects": sc.n_objects, "alphabet": args.alphabet, "rx": int(sc.rx.shape[0]),
                        "candidates": total, "max_order": 3, "iterations": args.iterations,
-                       "parallelism": f"dp{ws} (contiguous candidate shares)"},
+                       "parallelism": f"dp{ws} (contiguous candidate shares)",
+                       "records": ("none" if args.no_records else
+                                   "all-gathered to every rank" if args.gather and ws > 1 else
+                                   "sharded (kept on the rank that traced them)")},
             "orders": per_order, "valid_paths": res.valid, "gpu_launches": launches,
             "clocks": sampler.summary(),
         }
@@ -637,6 +640,9 @@ def main(argv=None):
     ap.add_argument("--alphabet", choices=("all", "walls"), default="all",
                     help="config3/4 objects: walls + edges (192) or the 64 walls only")
     ap.add_argument("--no-records", action="store_true", help="config3: counts only")
+    ap.add_argument("--gather", action="store_true",
+                    help="config3/4 under torchrun: all-gather every rank's path records (NCCL) "
+                         "inside the timed step; default keeps them sharded")
     ap.add_argument("--visibility", action="store_true",
                     help="config3/4: also flag occluded / wrong-side paths (fp_visibility_f64)")
     args = ap.parse_args(argv)

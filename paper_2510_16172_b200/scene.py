@@ -280,6 +280,31 @@ def reduce_sum_many(ts, world: int):
     return out
 
 
+def gather_rows(ts, world: int):
+    """All-gather per-rank row blocks of different lengths (the traced path
+    records: rx, sequence, T, L, points), concatenated in rank order on every
+    rank: the per-rank counts go first (one all_gather), then each field is
+    padded to the longest block and all-gathered (NCCL on GPU tensors, gloo in
+    the CPU tests). Identity for one rank."""
+    if world <= 1:
+        return list(ts)
+    dist = torch.distributed
+    dev = ts[0].device
+    n = torch.tensor([ts[0].shape[0]], dtype=torch.int64, device=dev)
+    counts = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(counts, n)
+    counts = [int(c.item()) for c in counts]
+    m = max(counts)
+    out = []
+    for t in ts:
+        pad = t.new_zeros((m,) + tuple(t.shape[1:]))
+        pad[:t.shape[0]] = t
+        bufs = [torch.empty_like(pad) for _ in range(world)]
+        dist.all_gather(bufs, pad)
+        out.append(torch.cat([b[:c] for b, c in zip(bufs, counts)]))
+    return out
+
+
 def decode_candidates(scene: UrbanScene, order: int, pattern: int, begin: int = 0, end: int | None = None):
     """(rx, sequence) of candidates [begin, end) of a (order, pattern) group, on the GPU."""
     lib = _lib.load()
@@ -335,7 +360,7 @@ def enumerate_candidates(num_objects: int, order: int, *, exclude_repeats: bool 
 def trace(scene: UrbanScene, max_order: int = 3, iterations: int = 20, fp_iters: int = 1,
           capacity: int | None = None, with_grad: bool = False, points: bool = False,
           rank: int | None = None, world: int | None = None, allreduce: bool = True,
-          device_scene: DeviceScene | None = None) -> TraceResult:
+          device_scene: DeviceScene | None = None, gather: bool = False) -> TraceResult:
     """Enumerate, solve and mask every candidate of order 1..max_order.
 
     capacity: records kept per order (default: all candidates of that order on
@@ -343,7 +368,10 @@ def trace(scene: UrbanScene, max_order: int = 3, iterations: int = 20, fp_iters:
     config-4 step (loss = sum 1/L^2 over valid paths and its gradient w.r.t.
     every object, TX and the wall vertices). Under torch.distributed, each
     rank takes a contiguous share of every group and (allreduce=True) the
-    counters and gradients are summed over ranks with NCCL.
+    counters and gradients are summed over ranks with NCCL; gather=True also
+    all-gathers every rank's path records (gather_rows), so each rank returns
+    the whole job's valid paths (rank-major; within a rank the compaction
+    order of the kernel). Otherwise records stay sharded.
     """
     lib = _lib.load()
     dist = torch.distributed
@@ -402,9 +430,13 @@ def trace(scene: UrbanScene, max_order: int = 3, iterations: int = 20, fp_iters:
     for k, rec in zip(range(1, max_order + 1), recs):
         cand, conv, inb, valid = (int(x) for x in total[k - 1].tolist())
         n_keep = min(int(local[k - 1, 3]), rec["cap"])
-        orders.append(OrderResult(k, cand, conv, inb, valid,
-                                  rec["rx"][:n_keep], rec["seq"][:n_keep], rec["T"][:n_keep],
-                                  rec["L"][:n_keep], rec["pts"][:n_keep] if points else None))
+        fields = [rec["rx"][:n_keep], rec["seq"][:n_keep], rec["T"][:n_keep], rec["L"][:n_keep]]
+        if points:
+            fields.append(rec["pts"][:n_keep])
+        if gather and allreduce:
+            fields = gather_rows(fields, world)
+        orders.append(OrderResult(k, cand, conv, inb, valid, *fields[:4],
+                                  fields[4] if points else None))
     res = TraceResult(orders)
     if with_grad:
         res.loss = float(grads["loss"].item())
