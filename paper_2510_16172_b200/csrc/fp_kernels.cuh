@@ -48,27 +48,50 @@ struct Outs {
   uint8_t* st;
 };
 
-// Widths (elements per path) of the staged slabs.
-template <int K>
+// Slab layout of one tile (kThreads paths) in shared memory, per op. Inputs:
+// basis, anchor, start, end, T (+ vT for OP_VJP), each a contiguous run of
+// records. Outputs (the same slab, after the inputs are in registers): only
+// the arrays the op can write — T, g (OP_SOLVE), points, L for solves;
+// the scene gradient (+ u for OP_VJP) for VJPs — then one status byte per
+// path.
+template <int K, int OP = OP_SOLVE_VJP>
 struct W {
   static constexpr int basis = 6 * K, anchor = 3 * K, vec = 3, T = 2 * K, pts = 3 * K;
-  static constexpr int in_elems = basis + anchor + 2 * vec + 2 * T;                   // + vT
-  static constexpr int out_elems = 2 * T + pts + 1 + basis + anchor + 2 * vec + T;  // T g pts len db da d0 d1 u
+  static constexpr bool has_v = OP == OP_VJP;
+  static constexpr bool w_T = OP != OP_VJP, w_g = OP == OP_SOLVE, w_pts = OP != OP_VJP,
+                        w_len = OP != OP_VJP, w_grad = OP != OP_SOLVE, w_u = OP == OP_VJP;
+  static constexpr int in_elems = basis + anchor + 2 * vec + T + (has_v ? T : 0);
+  static constexpr int oT = 0;
+  static constexpr int og = oT + (w_T ? T : 0);
+  static constexpr int oP = og + (w_g ? T : 0);
+  static constexpr int oL = oP + (w_pts ? pts : 0);
+  static constexpr int oDB = oL + (w_len ? 1 : 0);
+  static constexpr int oDA = oDB + (w_grad ? basis : 0);
+  static constexpr int oD0 = oDA + (w_grad ? anchor : 0);
+  static constexpr int oD1 = oD0 + (w_grad ? vec : 0);
+  static constexpr int oU = oD1 + (w_grad ? vec : 0);
+  static constexpr int out_elems = oU + (w_u ? T : 0);
   static constexpr int slab_elems = in_elems > out_elems ? in_elems : out_elems;
 };
 
-template <typename R, int K>
+// Bytes of one slab (+ status bytes), 128-byte aligned so two slabs stack.
+template <typename R, int K, int OP>
+constexpr size_t slab_bytes() {
+  return (size_t(W<K, OP>::slab_elems) * kThreads * sizeof(R) + kThreads + 127) / 128 * 128;
+}
+template <typename R, int K, int OP>
 constexpr size_t smem_bytes() {
-  return size_t(W<K>::slab_elems) * kThreads * sizeof(R) + kThreads + 16;
+  return slab_bytes<R, K, OP>();
 }
 
-extern __shared__ __align__(16) unsigned char fp_smem[];
+extern __shared__ __align__(128) unsigned char fp_smem[];
 
 // Output destinations of one path, computed only when results are written
 // (keeps ten 64-bit pointers out of the registers live across the solve).
-template <typename R, int K>
-__device__ __forceinline__ Outs<R> make_outs(const PathArgs<R>& a, int64_t row, int tid, bool staged) {
-  using Wk = W<K>;
+template <typename R, int K, int OP>
+__device__ __forceinline__ Outs<R> make_outs(const PathArgs<R>& a, int64_t row, int tid, bool staged,
+                                             unsigned char* slab) {
+  using Wk = W<K, OP>;
   Outs<R> o;
   if (!staged) {
     o.T = a.T_out ? a.T_out + row * Wk::T : nullptr;
@@ -83,25 +106,17 @@ __device__ __forceinline__ Outs<R> make_outs(const PathArgs<R>& a, int64_t row, 
     o.st = a.status_out ? a.status_out + row : nullptr;
     return o;
   }
-  R* oT = reinterpret_cast<R*>(fp_smem);
-  R* og = oT + kThreads * Wk::T;
-  R* op = og + kThreads * Wk::T;
-  R* ol = op + kThreads * Wk::pts;
-  R* odb = ol + kThreads;
-  R* oda = odb + kThreads * Wk::basis;
-  R* od0 = oda + kThreads * Wk::anchor;
-  R* od1 = od0 + kThreads * 3;
-  R* ou = od1 + kThreads * 3;
-  o.T = a.T_out ? oT + tid * Wk::T : nullptr;
-  o.g = a.g_out ? og + tid * Wk::T : nullptr;
-  o.pts = a.points_out ? op + tid * Wk::pts : nullptr;
-  o.len = a.length_out ? ol + tid : nullptr;
-  o.db = a.d_basis ? odb + tid * Wk::basis : nullptr;
-  o.da = a.d_anchor ? oda + tid * Wk::anchor : nullptr;
-  o.d0 = a.d_start ? od0 + tid * 3 : nullptr;
-  o.d1 = a.d_end ? od1 + tid * 3 : nullptr;
-  o.u = a.u_out ? ou + tid * Wk::T : nullptr;
-  o.st = reinterpret_cast<uint8_t*>(fp_smem + size_t(Wk::slab_elems) * kThreads * sizeof(R)) + tid;
+  R* sl = reinterpret_cast<R*>(slab);
+  o.T = (Wk::w_T && a.T_out) ? sl + kThreads * Wk::oT + tid * Wk::T : nullptr;
+  o.g = (Wk::w_g && a.g_out) ? sl + kThreads * Wk::og + tid * Wk::T : nullptr;
+  o.pts = (Wk::w_pts && a.points_out) ? sl + kThreads * Wk::oP + tid * Wk::pts : nullptr;
+  o.len = (Wk::w_len && a.length_out) ? sl + kThreads * Wk::oL + tid : nullptr;
+  o.db = (Wk::w_grad && a.d_basis) ? sl + kThreads * Wk::oDB + tid * Wk::basis : nullptr;
+  o.da = (Wk::w_grad && a.d_anchor) ? sl + kThreads * Wk::oDA + tid * Wk::anchor : nullptr;
+  o.d0 = (Wk::w_grad && a.d_start) ? sl + kThreads * Wk::oD0 + tid * 3 : nullptr;
+  o.d1 = (Wk::w_grad && a.d_end) ? sl + kThreads * Wk::oD1 + tid * 3 : nullptr;
+  o.u = (Wk::w_u && a.u_out) ? sl + kThreads * Wk::oU + tid * Wk::T : nullptr;
+  o.st = reinterpret_cast<uint8_t*>(slab + size_t(Wk::slab_elems) * kThreads * sizeof(R)) + tid;
   return o;
 }
 
@@ -141,9 +156,6 @@ __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t by
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
                "r"(smem_u32(src)), "r"(bytes)
                : "memory");
-}
-__device__ __forceinline__ void bulk_commit_and_wait_read() {
-  asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -186,7 +198,7 @@ __device__ __forceinline__ void load_rec(Rec<R, K>& r, const R* b, const R* a, c
 // ---- the per-path body -------------------------------------------------------
 template <typename R, int K, unsigned MASK, int OP>
 __device__ __forceinline__ void run_path(const PathArgs<R>& a, int64_t row, const Rec<R, K>& in,
-                                         bool has_v, int tid, bool staged) {
+                                         bool has_v, int tid, bool staged, unsigned char* slab) {
   using L = Lay<K, MASK>;
   constexpr int NA = L::NA;
   Geo<R, K> G;
@@ -215,7 +227,7 @@ __device__ __forceinline__ void run_path(const PathArgs<R>& a, int64_t row, cons
     tf[i][0] = P.T(L::idx(i, 0));
     tf[i][1] = L::plane(i) ? P.T(L::idx(i, 1)) : tin[i];
   }
-  const Outs<R> o = make_outs<R, K>(a, row, tid, staged);
+  const Outs<R> o = make_outs<R, K, OP>(a, row, tid, staged, slab);
   if (OP != OP_VJP) {
     if (o.T)
 #pragma unroll
@@ -305,21 +317,22 @@ constexpr int kInlineTileMaxOrder = 3;
 
 template <typename R, int K, int OP, unsigned M>
 __device__ __noinline__ void run_variant(const PathArgs<R>& a, int64_t row, const Rec<R, K>& in,
-                                         bool has_v, int tid) {
-  run_path<R, K, M, OP>(a, row, in, has_v, tid, true);
+                                         bool has_v, int tid, unsigned char* slab) {
+  run_path<R, K, M, OP>(a, row, in, has_v, tid, true, slab);
 }
 
 template <typename R, int K, int OP, unsigned M = 0>
 __device__ __forceinline__ void run_any_mask(unsigned m, const PathArgs<R>& a, int64_t row,
-                                             const Rec<R, K>& in, bool has_v, int tid) {
+                                             const Rec<R, K>& in, bool has_v, int tid,
+                                             unsigned char* slab) {
   if (m == M) {
     if constexpr (K <= kInlineTileMaxOrder)
-      run_path<R, K, M, OP>(a, row, in, has_v, tid, true);
+      run_path<R, K, M, OP>(a, row, in, has_v, tid, true, slab);
     else
-      run_variant<R, K, OP, M>(a, row, in, has_v, tid);
+      run_variant<R, K, OP, M>(a, row, in, has_v, tid, slab);
     return;
   }
-  if constexpr (M + 1 < (1u << K)) run_any_mask<R, K, OP, M + 1>(m, a, row, in, has_v, tid);
+  if constexpr (M + 1 < (1u << K)) run_any_mask<R, K, OP, M + 1>(m, a, row, in, has_v, tid, slab);
 }
 
 // Copy `width`-element records of the tile from global to shared memory with
@@ -357,59 +370,91 @@ __device__ __forceinline__ void tile_out(R* dst, const R* src, const int32_t* sr
   }
 }
 
-// One tile of up to kThreads paths: stage inputs in shared memory (TMA bulk
-// copies for full aligned contiguous tiles), compute in registers, stage the
-// outputs and write them back.
-template <typename R, int K, unsigned MASK, int OP>
-__device__ __forceinline__ void process_tile(const PathArgs<R>& a, const int32_t* srow, int64_t base,
-                                             int n, uint64_t* bar) {
-  using Wk = W<K>;
-  const int tid = threadIdx.x;
-  unsigned char* smem = fp_smem;
-  R* sb = reinterpret_cast<R*>(smem);
-  R* sa = sb + kThreads * Wk::basis;
-  R* s0 = sa + kThreads * Wk::anchor;
-  R* s1 = s0 + kThreads * 3;
-  R* sT = s1 + kThreads * 3;
-  R* sv = sT + kThreads * Wk::T;
-  const bool has_v = a.vT != nullptr;
-  bool tma = false;
-  if (srow == nullptr && n == kThreads) {
-    tma = aligned16(a.basis + base * Wk::basis) && aligned16(a.anchor + base * Wk::anchor) &&
-          aligned16(a.start + base * 3) && aligned16(a.end + base * 3) &&
-          aligned16(a.T + base * Wk::T) && (!has_v || aligned16(a.vT + base * Wk::T));
+// ---- one tile of up to kThreads paths ----------------------------------------
+// Input slab pointers of a tile (see W).
+template <typename R, int K, int OP>
+struct InSlab {
+  R *b, *a, *x0, *x1, *T, *v;
+  __device__ __forceinline__ explicit InSlab(unsigned char* slab) {
+    using Wk = W<K, OP>;
+    b = reinterpret_cast<R*>(slab);
+    a = b + kThreads * Wk::basis;
+    x0 = a + kThreads * Wk::anchor;
+    x1 = x0 + kThreads * 3;
+    T = x1 + kThreads * 3;
+    v = T + kThreads * Wk::T;
   }
-  if (tma) {
-    const uint32_t bb = kThreads * Wk::basis * sizeof(R), ba = kThreads * Wk::anchor * sizeof(R),
-                   bv = kThreads * 3 * sizeof(R), bt = kThreads * Wk::T * sizeof(R);
-    if (tid == 0) mbar_init(bar, 1);
-    __syncthreads();
-    if (tid == 0) {
-      mbar_expect_tx(bar, bb + ba + 2 * bv + bt + (has_v ? bt : 0));
-      bulk_g2s(sb, a.basis + base * Wk::basis, bb, bar);
-      bulk_g2s(sa, a.anchor + base * Wk::anchor, ba, bar);
-      bulk_g2s(s0, a.start + base * 3, bv, bar);
-      bulk_g2s(s1, a.end + base * 3, bv, bar);
-      bulk_g2s(sT, a.T + base * Wk::T, bt, bar);
-      if (has_v) bulk_g2s(sv, a.vT + base * Wk::T, bt, bar);
-    }
-    mbar_wait(bar, 0);
-  } else {
-    tile_in<R, Wk::basis>(sb, a.basis, srow, base, n);
-    tile_in<R, Wk::anchor>(sa, a.anchor, srow, base, n);
-    tile_in<R, 3>(s0, a.start, srow, base, n);
-    tile_in<R, 3>(s1, a.end, srow, base, n);
-    tile_in<R, Wk::T>(sT, a.T, srow, base, n);
-    if (has_v) tile_in<R, Wk::T>(sv, a.vT, srow, base, n);
-    cp_async_wait_all();
-    __syncthreads();
-  }
+};
 
-  // Registers take this thread's record; the slab is then reused for outputs.
+// Can the full contiguous tile at `base` move with TMA bulk copies (every
+// input / output run 16-byte aligned)?
+template <typename R, int K, int OP>
+__device__ __forceinline__ bool tile_in_aligned(const PathArgs<R>& a, int64_t base) {
+  using Wk = W<K, OP>;
+  return aligned16(a.basis + base * Wk::basis) && aligned16(a.anchor + base * Wk::anchor) &&
+         aligned16(a.start + base * 3) && aligned16(a.end + base * 3) &&
+         aligned16(a.T + base * Wk::T) && (!Wk::has_v || !a.vT || aligned16(a.vT + base * Wk::T));
+}
+template <typename R, int K, int OP>
+__device__ __forceinline__ bool tile_out_aligned(const PathArgs<R>& a, int64_t base) {
+  using Wk = W<K, OP>;
+  return (!a.T_out || aligned16(a.T_out + base * Wk::T)) && (!a.g_out || aligned16(a.g_out + base * Wk::T)) &&
+         (!a.points_out || aligned16(a.points_out + base * Wk::pts)) &&
+         (!a.length_out || aligned16(a.length_out + base)) &&
+         (!a.d_basis || aligned16(a.d_basis + base * Wk::basis)) &&
+         (!a.d_anchor || aligned16(a.d_anchor + base * Wk::anchor)) &&
+         (!a.d_start || aligned16(a.d_start + base * 3)) && (!a.d_end || aligned16(a.d_end + base * 3)) &&
+         (!a.u_out || aligned16(a.u_out + base * Wk::T)) && (!a.status_out || aligned16(a.status_out + base));
+}
+
+// One thread: TMA bulk loads of a full aligned tile into `slab`, completing on `bar`.
+template <typename R, int K, int OP>
+__device__ __forceinline__ void tile_load_tma(const PathArgs<R>& a, int64_t base, unsigned char* slab,
+                                              uint64_t* bar) {
+  using Wk = W<K, OP>;
+  const InSlab<R, K, OP> in(slab);
+  const bool has_v = Wk::has_v && a.vT != nullptr;
+  const uint32_t bb = kThreads * Wk::basis * sizeof(R), ba = kThreads * Wk::anchor * sizeof(R),
+                 bv = kThreads * 3 * sizeof(R), bt = kThreads * Wk::T * sizeof(R);
+  mbar_expect_tx(bar, bb + ba + 2 * bv + bt + (has_v ? bt : 0));
+  bulk_g2s(in.b, a.basis + base * Wk::basis, bb, bar);
+  bulk_g2s(in.a, a.anchor + base * Wk::anchor, ba, bar);
+  bulk_g2s(in.x0, a.start + base * 3, bv, bar);
+  bulk_g2s(in.x1, a.end + base * 3, bv, bar);
+  bulk_g2s(in.T, a.T + base * Wk::T, bt, bar);
+  if (has_v) bulk_g2s(in.v, a.vT + base * Wk::T, bt, bar);
+}
+
+// All threads: cp.async element copies of a partial / unaligned / gathered tile.
+template <typename R, int K, int OP>
+__device__ __forceinline__ void tile_load_async(const PathArgs<R>& a, const int32_t* srow, int64_t base,
+                                                int n, unsigned char* slab) {
+  using Wk = W<K, OP>;
+  const InSlab<R, K, OP> in(slab);
+  tile_in<R, Wk::basis>(in.b, a.basis, srow, base, n);
+  tile_in<R, Wk::anchor>(in.a, a.anchor, srow, base, n);
+  tile_in<R, 3>(in.x0, a.start, srow, base, n);
+  tile_in<R, 3>(in.x1, a.end, srow, base, n);
+  tile_in<R, Wk::T>(in.T, a.T, srow, base, n);
+  if (Wk::has_v && a.vT) tile_in<R, Wk::T>(in.v, a.vT, srow, base, n);
+  cp_async_wait_all();
+}
+
+// All threads, inputs staged in `slab`: each thread takes its record into
+// registers, the slab is reused for the outputs, every path is solved (its
+// own kind-mask variant under kAnyMask) and its results land in the slab.
+// Ends with the slab complete and visible to the TMA (async) proxy.
+template <typename R, int K, unsigned MASK, int OP>
+__device__ __forceinline__ void tile_compute(const PathArgs<R>& a, const int32_t* srow, int64_t base,
+                                             int n, unsigned char* slab) {
+  using Wk = W<K, OP>;
+  const int tid = threadIdx.x;
+  const bool has_v = Wk::has_v && a.vT != nullptr;
+  const InSlab<R, K, OP> sl(slab);
   Rec<R, K> in;
   if (tid < n)
-    load_rec(in, sb + tid * Wk::basis, sa + tid * Wk::anchor, s0 + tid * 3, s1 + tid * 3,
-             sT + tid * Wk::T, has_v ? sv + tid * Wk::T : nullptr);
+    load_rec(in, sl.b + tid * Wk::basis, sl.a + tid * Wk::anchor, sl.x0 + tid * 3, sl.x1 + tid * 3,
+             sl.T + tid * Wk::T, has_v ? sl.v + tid * Wk::T : nullptr);
   __syncthreads();
   if (tid < n) {
     const int64_t row = srow ? int64_t(srow[tid]) : base + tid;
@@ -420,63 +465,87 @@ __device__ __forceinline__ void process_tile(const PathArgs<R>& a, const int32_t
         if (__match_any_sync(act, m) != act && (tid & 31) == __ffs(act) - 1)
           atomicAdd(a.mixed_warps, 1ull);
       }
-      run_any_mask<R, K, OP>(m, a, row, in, has_v, tid);
+      run_any_mask<R, K, OP>(m, a, row, in, has_v, tid, slab);
     } else {
-      run_path<R, K, MASK, OP>(a, row, in, has_v, tid, true);
+      run_path<R, K, MASK, OP>(a, row, in, has_v, tid, true, slab);
     }
   }
   fence_async_smem();  // make the slab writes visible to the TMA (async) proxy
   __syncthreads();
+}
 
-  R* oT = reinterpret_cast<R*>(smem);
-  R* og = oT + kThreads * Wk::T;
-  R* op = og + kThreads * Wk::T;
-  R* ol = op + kThreads * Wk::pts;
-  R* odb = ol + kThreads;
-  R* oda = odb + kThreads * Wk::basis;
-  R* od0 = oda + kThreads * Wk::anchor;
-  R* od1 = od0 + kThreads * 3;
-  R* ou = od1 + kThreads * 3;
-  uint8_t* ost = reinterpret_cast<uint8_t*>(smem + size_t(Wk::slab_elems) * kThreads * sizeof(R));
-  // Full contiguous tiles with 16-byte aligned destinations leave with one TMA
-  // bulk store per slab; others with cooperative (scattering) stores.
-  if (srow == nullptr && n == kThreads &&
-      (!a.T_out || aligned16(a.T_out + base * Wk::T)) && (!a.g_out || aligned16(a.g_out + base * Wk::T)) &&
-      (!a.points_out || aligned16(a.points_out + base * Wk::pts)) &&
-      (!a.length_out || aligned16(a.length_out + base)) &&
-      (!a.d_basis || aligned16(a.d_basis + base * Wk::basis)) &&
-      (!a.d_anchor || aligned16(a.d_anchor + base * Wk::anchor)) &&
-      (!a.d_start || aligned16(a.d_start + base * 3)) && (!a.d_end || aligned16(a.d_end + base * 3)) &&
-      (!a.u_out || aligned16(a.u_out + base * Wk::T)) &&
-      (!a.status_out || aligned16(a.status_out + base))) {
+// One thread: TMA bulk stores of a full aligned tile's output runs (committed
+// as one bulk group; the caller waits for the reads before reusing the slab).
+template <typename R, int K, int OP>
+__device__ __forceinline__ void tile_store_tma(const PathArgs<R>& a, int64_t base, unsigned char* slab) {
+  using Wk = W<K, OP>;
+  R* sl = reinterpret_cast<R*>(slab);
+  uint8_t* ost = slab + size_t(Wk::slab_elems) * kThreads * sizeof(R);
+  constexpr uint32_t bT = kThreads * Wk::T * sizeof(R), bP = kThreads * Wk::pts * sizeof(R),
+                     bL = kThreads * sizeof(R), bB = kThreads * Wk::basis * sizeof(R),
+                     bA = kThreads * Wk::anchor * sizeof(R), bV = kThreads * 3 * sizeof(R);
+  if (Wk::w_T && a.T_out) bulk_s2g(a.T_out + base * Wk::T, sl + kThreads * Wk::oT, bT);
+  if (Wk::w_g && a.g_out) bulk_s2g(a.g_out + base * Wk::T, sl + kThreads * Wk::og, bT);
+  if (Wk::w_pts && a.points_out) bulk_s2g(a.points_out + base * Wk::pts, sl + kThreads * Wk::oP, bP);
+  if (Wk::w_len && a.length_out) bulk_s2g(a.length_out + base, sl + kThreads * Wk::oL, bL);
+  if (Wk::w_grad && a.d_basis) bulk_s2g(a.d_basis + base * Wk::basis, sl + kThreads * Wk::oDB, bB);
+  if (Wk::w_grad && a.d_anchor) bulk_s2g(a.d_anchor + base * Wk::anchor, sl + kThreads * Wk::oDA, bA);
+  if (Wk::w_grad && a.d_start) bulk_s2g(a.d_start + base * 3, sl + kThreads * Wk::oD0, bV);
+  if (Wk::w_grad && a.d_end) bulk_s2g(a.d_end + base * 3, sl + kThreads * Wk::oD1, bV);
+  if (Wk::w_u && a.u_out) bulk_s2g(a.u_out + base * Wk::T, sl + kThreads * Wk::oU, bT);
+  if (a.status_out) bulk_s2g(a.status_out + base, ost, kThreads);
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_all() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+// All threads: cooperative (scattering) stores of a partial / gathered tile.
+template <typename R, int K, int OP>
+__device__ __forceinline__ void tile_store_coop(const PathArgs<R>& a, const int32_t* srow, int64_t base,
+                                                int n, unsigned char* slab) {
+  using Wk = W<K, OP>;
+  R* sl = reinterpret_cast<R*>(slab);
+  uint8_t* ost = slab + size_t(Wk::slab_elems) * kThreads * sizeof(R);
+  if (Wk::w_T && a.T_out) tile_out<R, Wk::T>(a.T_out, sl + kThreads * Wk::oT, srow, base, n);
+  if (Wk::w_g && a.g_out) tile_out<R, Wk::T>(a.g_out, sl + kThreads * Wk::og, srow, base, n);
+  if (Wk::w_pts && a.points_out) tile_out<R, Wk::pts>(a.points_out, sl + kThreads * Wk::oP, srow, base, n);
+  if (Wk::w_len && a.length_out) tile_out<R, 1>(a.length_out, sl + kThreads * Wk::oL, srow, base, n);
+  if (Wk::w_grad && a.d_basis) tile_out<R, Wk::basis>(a.d_basis, sl + kThreads * Wk::oDB, srow, base, n);
+  if (Wk::w_grad && a.d_anchor) tile_out<R, Wk::anchor>(a.d_anchor, sl + kThreads * Wk::oDA, srow, base, n);
+  if (Wk::w_grad && a.d_start) tile_out<R, 3>(a.d_start, sl + kThreads * Wk::oD0, srow, base, n);
+  if (Wk::w_grad && a.d_end) tile_out<R, 3>(a.d_end, sl + kThreads * Wk::oD1, srow, base, n);
+  if (Wk::w_u && a.u_out) tile_out<R, Wk::T>(a.u_out, sl + kThreads * Wk::oU, srow, base, n);
+  if (a.status_out) tile_out<uint8_t, 1>(a.status_out, ost, srow, base, n);
+}
+
+// One tile per CTA: stage inputs (TMA bulk copies for full aligned contiguous
+// tiles, cp.async otherwise), compute in registers, stage the outputs and
+// write them back (TMA bulk stores when full and aligned).
+template <typename R, int K, unsigned MASK, int OP>
+__device__ __forceinline__ void process_tile(const PathArgs<R>& a, const int32_t* srow, int64_t base,
+                                             int n, uint64_t* bar) {
+  const int tid = threadIdx.x;
+  unsigned char* slab = fp_smem;
+  const bool full = srow == nullptr && n == kThreads;
+  if (full && tile_in_aligned<R, K, OP>(a, base)) {
+    if (tid == 0) mbar_init(bar, 1);
+    __syncthreads();
+    if (tid == 0) tile_load_tma<R, K, OP>(a, base, slab, bar);
+    mbar_wait(bar, 0);
+  } else {
+    tile_load_async<R, K, OP>(a, srow, base, n, slab);
+    __syncthreads();
+  }
+  tile_compute<R, K, MASK, OP>(a, srow, base, n, slab);
+  if (full && tile_out_aligned<R, K, OP>(a, base)) {
     if (tid == 0) {
-      constexpr uint32_t bT = kThreads * Wk::T * sizeof(R), bP = kThreads * Wk::pts * sizeof(R),
-                         bL = kThreads * sizeof(R), bB = kThreads * Wk::basis * sizeof(R),
-                         bA = kThreads * Wk::anchor * sizeof(R), bV = kThreads * 3 * sizeof(R);
-      if (a.T_out) bulk_s2g(a.T_out + base * Wk::T, oT, bT);
-      if (a.g_out) bulk_s2g(a.g_out + base * Wk::T, og, bT);
-      if (a.points_out) bulk_s2g(a.points_out + base * Wk::pts, op, bP);
-      if (a.length_out) bulk_s2g(a.length_out + base, ol, bL);
-      if (a.d_basis) bulk_s2g(a.d_basis + base * Wk::basis, odb, bB);
-      if (a.d_anchor) bulk_s2g(a.d_anchor + base * Wk::anchor, oda, bA);
-      if (a.d_start) bulk_s2g(a.d_start + base * 3, od0, bV);
-      if (a.d_end) bulk_s2g(a.d_end + base * 3, od1, bV);
-      if (a.u_out) bulk_s2g(a.u_out + base * Wk::T, ou, bT);
-      if (a.status_out) bulk_s2g(a.status_out + base, ost, kThreads);
-      bulk_commit_and_wait_read();
+      tile_store_tma<R, K, OP>(a, base, slab);
+      bulk_wait_read_all();
     }
     return;
   }
-  if (a.T_out) tile_out<R, Wk::T>(a.T_out, oT, srow, base, n);
-  if (a.g_out) tile_out<R, Wk::T>(a.g_out, og, srow, base, n);
-  if (a.points_out) tile_out<R, Wk::pts>(a.points_out, op, srow, base, n);
-  if (a.length_out) tile_out<R, 1>(a.length_out, ol, srow, base, n);
-  if (a.d_basis) tile_out<R, Wk::basis>(a.d_basis, odb, srow, base, n);
-  if (a.d_anchor) tile_out<R, Wk::anchor>(a.d_anchor, oda, srow, base, n);
-  if (a.d_start) tile_out<R, 3>(a.d_start, od0, srow, base, n);
-  if (a.d_end) tile_out<R, 3>(a.d_end, od1, srow, base, n);
-  if (a.u_out) tile_out<R, Wk::T>(a.u_out, ou, srow, base, n);
-  if (a.status_out) tile_out<uint8_t, 1>(a.status_out, ost, srow, base, n);
+  tile_store_coop<R, K, OP>(a, srow, base, n, slab);
 }
 
 // Minimum co-resident CTAs per SM requested from ptxas (caps registers at
@@ -552,7 +621,7 @@ template <typename R, int K, unsigned MASK, int OP>
 cudaError_t launch_path_impl(const PathArgs<R>& a, cudaStream_t stream) {
   const int64_t rows = a.rows ? a.n_rows : a.B - a.row_begin;
   if (rows <= 0) return cudaSuccess;
-  const size_t smem = smem_bytes<R, K>();
+  constexpr size_t smem = smem_bytes<R, K, OP>();
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(path_kernel<R, K, MASK, OP>,
