@@ -368,20 +368,55 @@ def run_ours(args):
             if rc:
                 _lib.check(rc, "fp_solve_vjp_host_f32")
 
+        # Streaming through the public submit / wait API: step i + 1 is
+        # submitted before step i is waited for, so its host-to-device copies
+        # overlap step i's device-to-host copies (two output sets in flight).
+        # Every step still copies its inputs in and its results out.
+        hout2 = [hout, [pin(tuple(t.shape), t.dtype) for t in hout]]
+        import ctypes
+
+        def e2e_submit(i):
+            tk = ctypes.c_uint64(0)
+            rc = lib.fp_solve_vjp_host_submit_f32(*(P(t) for t in hin), B, K, I, F, 1.0, _lib.VJP_FULL,
+                                                  *(P(t) for t in hout2[i % 2]), args.stream_chunk, 2,
+                                                  ctypes.addressof(tk))
+            if rc:
+                _lib.check(rc, "fp_solve_vjp_host_submit_f32")
+            return tk.value
+
+        def e2e_wait(tk):
+            _lib.check(lib.fp_host_wait(tk), "fp_host_wait")
+
         e2e_step()
         _barrier(ws)
         e_steps = max(3, args.steps // 4)
         t0 = time.perf_counter()
         for _ in range(e_steps):
             e2e_step()
-        e_s = (time.perf_counter() - t0) / e_steps
-        e_s = _max_over_ranks(e_s, ws, dev)
-        e_conv = int(((hout[7] & _lib.STATUS_UNCONVERGED_MASK) == 0).sum().item())
+        e_blocking_s = _max_over_ranks((time.perf_counter() - t0) / e_steps, ws, dev)
+        e2e_wait(e2e_submit(0))
+        _barrier(ws)
+        t0 = time.perf_counter()
+        prev = None
+        for i in range(e_steps):
+            tk = e2e_submit(i)
+            if prev is not None:
+                e2e_wait(prev)
+            prev = tk
+        e2e_wait(prev)
+        e_s = _max_over_ranks((time.perf_counter() - t0) / e_steps, ws, dev)
+        e_conv = int(((hout2[(e_steps - 1) % 2][7] & _lib.STATUS_UNCONVERGED_MASK) == 0).sum().item())
         e2e = {"value": _sum_over_ranks(e_conv, ws, dev) / e_s, "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": e_s * 1e3, "raw_paths_per_s": paths_all / e_s,
-               "path": "fp_solve_vjp_host_f32 (pinned host buffers; copy-in, compute and copy-out "
-                       f"streams over 3 device chunk slots of {args.chunk} paths)"}
+               "path": ("fp_solve_vjp_host_submit_f32 + fp_host_wait (pinned host buffers; steps "
+                        "submitted back to back, each waited one step later; copy-in, compute and "
+                        f"copy-out streams over 2 device chunk slots of up to {args.stream_chunk} "
+                        "paths)"),
+               "blocking": {"ms_per_step": e_blocking_s * 1e3,
+                            "value": _sum_over_ranks(e_conv, ws, dev) / e_blocking_s,
+                            "path": ("fp_solve_vjp_host_f32 (one blocking call per step; chunks of "
+                                     f"{args.chunk} paths over 3 slots)")}}
 
     # ---- CPU baseline (rank 0, N=1 only) ----------------------------------------------
     cpu = None
@@ -629,7 +664,9 @@ def main(argv=None):
     ap.add_argument("--iterations", type=int, default=20)
     ap.add_argument("--paths", type=int, default=1 << 22, help="paths per GPU")
     ap.add_argument("--sample", type=int, default=1 << 17, help="CPU baseline sample size")
-    ap.add_argument("--chunk", type=int, default=1 << 19, help="e2e pipeline chunk (paths)")
+    ap.add_argument("--chunk", type=int, default=1 << 19, help="e2e blocking call: pipeline chunk (paths)")
+    ap.add_argument("--stream-chunk", type=int, default=1 << 22,
+                    help="e2e submitted steps: pipeline chunk (paths; tools/e2e_pipe_sweep.py)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="tiny CPU samples (debugging)")

@@ -130,6 +130,26 @@ int fp_solve_vjp_host_f64(const double* basis, const double* anchor, const doubl
                           double* points_out, double* length_out, double* d_basis,
                           double* d_anchor, double* d_start, double* d_end, uint8_t* status_out,
                           int64_t chunk, int depth);
+/* The same call without the final wait: enqueues the copies and kernels and
+ * returns a ticket; fp_host_wait(ticket) blocks until that call's outputs are
+ * in host memory. Consecutive calls with the same order and chunk chain
+ * through one ring of chunk slots, so call i + 1's host-to-device copies
+ * overlap call i's device-to-host copies. The host buffers of a submitted
+ * call must stay valid and unmodified until its wait returns; at most 16
+ * calls are in flight (a submit waits for the one 16 tickets back). */
+int fp_solve_vjp_host_submit_f32(const float* basis, const float* anchor, const float* start,
+                                 const float* end, const float* T0, int64_t B, int K, int iterations,
+                                 int fp_iters, float w_L_scale, int mode, float* T_out,
+                                 float* points_out, float* length_out, float* d_basis,
+                                 float* d_anchor, float* d_start, float* d_end, uint8_t* status_out,
+                                 int64_t chunk, int depth, uint64_t* ticket);
+int fp_solve_vjp_host_submit_f64(const double* basis, const double* anchor, const double* start,
+                                 const double* end, const double* T0, int64_t B, int K,
+                                 int iterations, int fp_iters, double w_L_scale, int mode,
+                                 double* T_out, double* points_out, double* length_out,
+                                 double* d_basis, double* d_anchor, double* d_start, double* d_end,
+                                 uint8_t* status_out, int64_t chunk, int depth, uint64_t* ticket);
+int fp_host_wait(uint64_t ticket);
 
 /* ---- objective pieces: objective.path_length / gradient / hessian
  * (objective.py:34-64), unclamped norms; degenerate segments flag

@@ -66,6 +66,9 @@ _SIGS = {
     "fp_solve_vjp_f64": [_P] * 5 + [_I64, _I, _I, _I, _P, _D, _I] + [_P] * 8 + [_P],
     "fp_solve_vjp_host_f32": [_P] * 5 + [_I64, _I, _I, _I, _F, _I] + [_P] * 8 + [_I64, _I],
     "fp_solve_vjp_host_f64": [_P] * 5 + [_I64, _I, _I, _I, _D, _I] + [_P] * 8 + [_I64, _I],
+    "fp_solve_vjp_host_submit_f32": [_P] * 5 + [_I64, _I, _I, _I, _F, _I] + [_P] * 8 + [_I64, _I, _P],
+    "fp_solve_vjp_host_submit_f64": [_P] * 5 + [_I64, _I, _I, _I, _D, _I] + [_P] * 8 + [_I64, _I, _P],
+    "fp_host_wait": [C.c_uint64],
     "fp_objective_f64": [_P] * 5 + [_I64, _I] + [_P] * 4 + [_P],
     "fp_line_search_f64": [_P] * 7 + [_I64, _I, _I] + [_P] * 2 + [_P],
     "fp_init_params_f64": [_P] * 4 + [_I64, _I, _P, _P],

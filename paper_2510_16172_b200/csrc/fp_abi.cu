@@ -565,7 +565,19 @@ struct HostPipe {
   std::vector<void*> bufs;
   size_t buf_bytes = 0;
   int device = -1;
+  int64_t chunks = 0;   // chunks enqueued since setup: the ring position carries across calls
+  uint64_t layout = 0;  // slot layout of the last call (order, chunk, element size)
+  // Completion of submitted calls: ticket t records on job_ev[t % kJobs];
+  // at most kJobs calls are in flight (a submit first waits for ticket t - kJobs).
+  static constexpr int kJobs = 16;
+  cudaEvent_t job_ev[kJobs] = {};
+  uint64_t next_ticket = 1;
+  void drain() {
+    for (cudaStream_t s : {s_in, s_k, s_out})
+      if (s) cudaStreamSynchronize(s);
+  }
   void release() {
+    drain();
     for (void* p : bufs) cudaFree(p);
     for (auto* v : {&ev_in, &ev_k, &ev_out})
       for (cudaEvent_t e : *v) cudaEventDestroy(e);
@@ -578,6 +590,8 @@ struct HostPipe {
     s_in = s_k = s_out = nullptr;
     buf_bytes = 0;
     device = -1;
+    chunks = 0;
+    layout = 0;
   }
   cudaError_t setup(int dev, int depth, size_t slot) {
     release();
@@ -612,10 +626,12 @@ static cudaError_t copy_arrays(void** dst, void** src, size_t* bytes, size_t n, 
 }
 
 template <typename R>
-static int host_pipeline(const R* basis, const R* anchor, const R* start, const R* end, const R* T0,
-                         int64_t B, int K, int iterations, int fp_iters, R w_L_scale, int mode,
-                         R* T_out, R* points_out, R* length_out, R* d_basis, R* d_anchor,
-                         R* d_start, R* d_end, uint8_t* status_out, int64_t chunk, int depth) {
+static int host_submit(const R* basis, const R* anchor, const R* start, const R* end, const R* T0,
+                       int64_t B, int K, int iterations, int fp_iters, R w_L_scale, int mode,
+                       R* T_out, R* points_out, R* length_out, R* d_basis, R* d_anchor,
+                       R* d_start, R* d_end, uint8_t* status_out, int64_t chunk, int depth,
+                       uint64_t* ticket) {
+  if (ticket) *ticket = 0;  // 0: nothing in flight
   if (B < 0 || iterations < 1 || fp_iters < 1 || depth < 1 || depth > 8)
     return FP_ERR_INVALID_ARGUMENT;
   if (K < 0 || K > FP_MAX_ORDER) return FP_ERR_UNSUPPORTED_ORDER;
@@ -638,6 +654,14 @@ static int host_pipeline(const R* basis, const R* anchor, const R* start, const 
       g_pipe.release();
       return cuda_status(e);
     }
+  }
+  // Calls with the same slot layout chain through the ring (the event waits
+  // below keep every region's reuse ordered); a layout change first lets the
+  // previous calls finish, since their input and output regions differ.
+  const uint64_t layout = (uint64_t(K) << 48) ^ (uint64_t(chunk) << 8) ^ sizeof(R);
+  if (g_pipe.layout != layout) {
+    g_pipe.drain();
+    g_pipe.layout = layout;
   }
   const R* hin[5] = {basis, anchor, start, end, T0};
   R* hout[7] = {T_out, points_out, length_out, d_basis, d_anchor, d_start, d_end};
@@ -668,7 +692,7 @@ static int host_pipeline(const R* basis, const R* anchor, const R* start, const 
   // next call reuses (or reallocates) the slots.
   auto enqueue = [&]() -> int {
     cudaError_t e;
-    int64_t c = 0, lo = 0;
+    int64_t c = g_pipe.chunks, lo = 0;
     for (const int64_t n : sizes) {
       const int j = int(c % depth);
       char* p = static_cast<char*>(g_pipe.bufs[j]);
@@ -735,15 +759,39 @@ static int host_pipeline(const R* basis, const R* anchor, const R* start, const 
       if ((e = cudaEventRecord(g_pipe.ev_out[j], s_out)) != cudaSuccess) return cuda_status(e);
       lo += n;
       ++c;
+      g_pipe.chunks = c;
     }
     return FP_OK;
   };
   int rc = enqueue();
-  for (cudaStream_t s : {s_in, s_k, s_out}) {
-    const cudaError_t se = cudaStreamSynchronize(s);
-    if (se != cudaSuccess && rc == FP_OK) rc = cuda_status(se);
+  if (rc != FP_OK) {
+    g_pipe.drain();
+    return rc;
   }
-  return rc;
+  // completion ticket: an event after this call's last copy-out
+  const uint64_t t = g_pipe.next_ticket++;
+  cudaEvent_t& ev = g_pipe.job_ev[t % HostPipe::kJobs];
+  if (ev == nullptr) {
+    if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return cuda_status(e);
+  } else if ((e = cudaEventSynchronize(ev)) != cudaSuccess) {  // ticket t - kJobs
+    return cuda_status(e);
+  }
+  if ((e = cudaEventRecord(ev, s_out)) != cudaSuccess) return cuda_status(e);
+  if (ticket) *ticket = t;
+  return FP_OK;
+}
+
+// Wait until the outputs of submitted call `ticket` are in host memory.
+static int host_wait(uint64_t ticket) {
+  if (ticket == 0) return FP_OK;
+  cudaEvent_t ev = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(g_pipe.mu);
+    if (ticket >= g_pipe.next_ticket) return FP_ERR_INVALID_ARGUMENT;
+    if (ticket + HostPipe::kJobs < g_pipe.next_ticket) return FP_OK;  // its slot was reused: done
+    ev = g_pipe.job_ev[ticket % HostPipe::kJobs];
+  }
+  return cuda_status(cudaEventSynchronize(ev));
 }
 
 }  // namespace fp
@@ -809,9 +857,11 @@ int fp_solve_vjp_host_f32(const float* basis, const float* anchor, const float* 
                           int fp_iters, float w_L_scale, int mode, float* T_out, float* points_out,
                           float* length_out, float* d_basis, float* d_anchor, float* d_start,
                           float* d_end, uint8_t* status_out, int64_t chunk, int depth) {
-  return host_pipeline<float>(basis, anchor, start, end, T0, B, K, iterations, fp_iters, w_L_scale,
-                              mode, T_out, points_out, length_out, d_basis, d_anchor, d_start, d_end,
-                              status_out, chunk, depth);
+  uint64_t t = 0;
+  const int rc = host_submit<float>(basis, anchor, start, end, T0, B, K, iterations, fp_iters,
+                                    w_L_scale, mode, T_out, points_out, length_out, d_basis, d_anchor,
+                                    d_start, d_end, status_out, chunk, depth, &t);
+  return rc != FP_OK ? rc : host_wait(t);
 }
 
 int fp_solve_vjp_host_f64(const double* basis, const double* anchor, const double* start,
@@ -820,10 +870,38 @@ int fp_solve_vjp_host_f64(const double* basis, const double* anchor, const doubl
                           double* points_out, double* length_out, double* d_basis,
                           double* d_anchor, double* d_start, double* d_end, uint8_t* status_out,
                           int64_t chunk, int depth) {
-  return host_pipeline<double>(basis, anchor, start, end, T0, B, K, iterations, fp_iters, w_L_scale,
-                               mode, T_out, points_out, length_out, d_basis, d_anchor, d_start,
-                               d_end, status_out, chunk, depth);
+  uint64_t t = 0;
+  const int rc = host_submit<double>(basis, anchor, start, end, T0, B, K, iterations, fp_iters,
+                                     w_L_scale, mode, T_out, points_out, length_out, d_basis,
+                                     d_anchor, d_start, d_end, status_out, chunk, depth, &t);
+  return rc != FP_OK ? rc : host_wait(t);
 }
+
+int fp_solve_vjp_host_submit_f32(const float* basis, const float* anchor, const float* start,
+                                 const float* end, const float* T0, int64_t B, int K, int iterations,
+                                 int fp_iters, float w_L_scale, int mode, float* T_out,
+                                 float* points_out, float* length_out, float* d_basis,
+                                 float* d_anchor, float* d_start, float* d_end, uint8_t* status_out,
+                                 int64_t chunk, int depth, uint64_t* ticket) {
+  if (ticket == nullptr) return FP_ERR_INVALID_ARGUMENT;
+  return host_submit<float>(basis, anchor, start, end, T0, B, K, iterations, fp_iters, w_L_scale,
+                            mode, T_out, points_out, length_out, d_basis, d_anchor, d_start, d_end,
+                            status_out, chunk, depth, ticket);
+}
+
+int fp_solve_vjp_host_submit_f64(const double* basis, const double* anchor, const double* start,
+                                 const double* end, const double* T0, int64_t B, int K,
+                                 int iterations, int fp_iters, double w_L_scale, int mode,
+                                 double* T_out, double* points_out, double* length_out,
+                                 double* d_basis, double* d_anchor, double* d_start, double* d_end,
+                                 uint8_t* status_out, int64_t chunk, int depth, uint64_t* ticket) {
+  if (ticket == nullptr) return FP_ERR_INVALID_ARGUMENT;
+  return host_submit<double>(basis, anchor, start, end, T0, B, K, iterations, fp_iters, w_L_scale,
+                             mode, T_out, points_out, length_out, d_basis, d_anchor, d_start, d_end,
+                             status_out, chunk, depth, ticket);
+}
+
+int fp_host_wait(uint64_t ticket) { return host_wait(ticket); }
 
 int fp_objective_f64(const double* basis, const double* anchor, const double* start,
                      const double* end, const double* T, int64_t B, int K, double* length_out,

@@ -157,21 +157,22 @@ def solve_with_gradients(scene: BatchScene, T0=None, opts: SolveOptions = SolveO
     return res, grads
 
 
-def solve_with_gradients_host(basis, anchor, start, end, T0=None, iterations: int = 20,
-                              fixed_point_iters: int = 1, weight: float = 1.0, mode: str = "full",
-                              chunk: int = 1 << 19, depth: int = 3, out=None,
-                              precision: Precision | None = None):
-    """solve_with_gradients for host (numpy) arrays in the reference layout.
+class HostJob:
+    """A submitted host-buffer step (`submit_with_gradients_host`); `wait()`
+    blocks until its outputs are in host memory and returns them."""
 
-    One call of fp_solve_vjp_host_f32 / _f64: the batch streams through the
-    GPU in chunks (copy-in, compute and copy-out streams over a ring of
-    `depth` device chunk slots), so both PCIe directions and compute overlap.
-    `precision` defaults to the dtype of `basis` (float64 arrays run the fp64
-    kernels, never a silent fp32 downcast). Pinned (page-locked) arrays
-    transfer fastest: pass `out` from `host_buffers` to reuse pinned outputs.
-    Returns a dict of numpy arrays: T, points, length, status, d_basis,
-    d_anchor, d_start, d_end.
-    """
+    def __init__(self, ticket: int, out: dict, keep: tuple):
+        self.ticket, self.out, self._keep = ticket, out, keep  # keep inputs alive until waited
+
+    def wait(self) -> dict:
+        if self._keep is not None:
+            _lib.check(_lib.load().fp_host_wait(self.ticket), "fp_host_wait")
+            self._keep = None
+        return self.out
+
+
+def _host_call(submit: bool, basis, anchor, start, end, T0, iterations, fixed_point_iters, weight,
+               mode, chunk, depth, out, precision):
     lib = _lib.load()
     if precision is None:
         precision = Precision.DOUBLE if np.asarray(basis).dtype == np.float64 else Precision.SINGLE
@@ -192,14 +193,56 @@ def solve_with_gradients_host(basis, anchor, start, end, T0=None, iterations: in
         if v.dtype != want or not v.flags.c_contiguous:
             raise ShapeMismatch(f"out[{k!r}] must be a C-contiguous {np.dtype(want).name} array")
     P = lambda a: a.ctypes.data  # noqa: E731
-    name = "fp_solve_vjp_host_f32" if precision is Precision.SINGLE else "fp_solve_vjp_host_f64"
-    rc = getattr(lib, name)(P(basis), P(anchor), P(start), P(end), P(T0), B, K, iterations,
-                            fixed_point_iters, float(weight), _MODES[mode], P(out["T"]),
-                            P(out["points"]), P(out["length"]), P(out["d_basis"]),
-                            P(out["d_anchor"]), P(out["d_start"]), P(out["d_end"]),
-                            P(out["status"]), int(chunk), int(depth))
-    _lib.check(rc, name)
-    return out
+    single = precision is Precision.SINGLE
+    args = (P(basis), P(anchor), P(start), P(end), P(T0), B, K, iterations, fixed_point_iters,
+            float(weight), _MODES[mode], P(out["T"]), P(out["points"]), P(out["length"]),
+            P(out["d_basis"]), P(out["d_anchor"]), P(out["d_start"]), P(out["d_end"]),
+            P(out["status"]), int(chunk), int(depth))
+    if not submit:
+        name = "fp_solve_vjp_host_f32" if single else "fp_solve_vjp_host_f64"
+        _lib.check(getattr(lib, name)(*args), name)
+        return out
+    import ctypes
+
+    ticket = ctypes.c_uint64(0)
+    name = "fp_solve_vjp_host_submit_f32" if single else "fp_solve_vjp_host_submit_f64"
+    _lib.check(getattr(lib, name)(*args, ctypes.addressof(ticket)), name)
+    return HostJob(int(ticket.value), out, (basis, anchor, start, end, T0))
+
+
+def solve_with_gradients_host(basis, anchor, start, end, T0=None, iterations: int = 20,
+                              fixed_point_iters: int = 1, weight: float = 1.0, mode: str = "full",
+                              chunk: int = 1 << 19, depth: int = 3, out=None,
+                              precision: Precision | None = None):
+    """solve_with_gradients for host (numpy) arrays in the reference layout.
+
+    One call of fp_solve_vjp_host_f32 / _f64: the batch streams through the
+    GPU in chunks (copy-in, compute and copy-out streams over a ring of
+    `depth` device chunk slots), so both PCIe directions and compute overlap.
+    `precision` defaults to the dtype of `basis` (float64 arrays run the fp64
+    kernels, never a silent fp32 downcast). Pinned (page-locked) arrays
+    transfer fastest: pass `out` from `host_buffers` to reuse pinned outputs.
+    Returns a dict of numpy arrays: T, points, length, status, d_basis,
+    d_anchor, d_start, d_end.
+    """
+    return _host_call(False, basis, anchor, start, end, T0, iterations, fixed_point_iters, weight,
+                      mode, chunk, depth, out, precision)
+
+
+def submit_with_gradients_host(basis, anchor, start, end, T0=None, iterations: int = 20,
+                               fixed_point_iters: int = 1, weight: float = 1.0, mode: str = "full",
+                               chunk: int = 1 << 19, depth: int = 3, out=None,
+                               precision: Precision | None = None) -> HostJob:
+    """solve_with_gradients_host without the final wait: returns a HostJob.
+
+    Consecutive submits (same order and chunk) chain through one ring of
+    device chunk slots, so step i + 1's host-to-device copies overlap step
+    i's device-to-host copies (fp_solve_vjp_host_submit_*). The input and
+    output arrays must stay untouched until `job.wait()` returns; use one
+    `out` set per step in flight.
+    """
+    return _host_call(True, basis, anchor, start, end, T0, iterations, fixed_point_iters, weight,
+                      mode, chunk, depth, out, precision)
 
 
 def host_buffers(B: int, K: int, pinned: bool = True, precision: Precision = Precision.SINGLE) -> dict:

@@ -77,3 +77,13 @@ def test_enumerate_candidates_argument_checks():
         enumerate_candidates(5, 2, begin=0, end=5 * 4 + 1)
     with pytest.raises(ValueError):
         enumerate_candidates(5, 2, exclude_repeats=False, begin=3, end=2)
+
+
+def test_host_submit_and_wait_argument_checks():
+    lib = _lib.load()
+    null = None
+    # a submit needs somewhere to put its ticket; empty batches complete at once
+    assert lib.fp_solve_vjp_host_submit_f32(*([null] * 5), 4, 2, 20, 1, 1.0, 0, *([null] * 8), 0, 3,
+                                            null) == 1
+    assert lib.fp_host_wait(0) == 0
+    assert lib.fp_host_wait(1 << 40) == 1  # never issued

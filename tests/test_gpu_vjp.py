@@ -199,3 +199,25 @@ def test_host_pipeline_fp64_equals_device_step(K, chunk):
                           ("status", res.status), ("d_basis", grads.basis), ("d_anchor", grads.anchor),
                           ("d_start", grads.start), ("d_end", grads.end)):
             assert np.array_equal(out[name], dev.cpu().numpy()), (name, pinned)
+
+
+def test_host_submit_chain_equals_device_step():
+    """Submitted host-buffer steps chain through one slot ring: several in
+    flight (step i + 1's copies overlap step i's), a change of order in
+    between (the ring drains), each result bitwise the device step's."""
+    from paper_2510_16172_b200.solver import host_buffers, submit_with_gradients_host
+
+    ref, jobs = {}, []
+    for K in (3, 3, 2, 3):
+        b = datagen.gen_batch(80 + K, datagen.all_orderings(K), 700 // 2 ** K + 9)
+        sc = BatchScene(b.basis, b.anchor, b.start, b.end)
+        res, grads = solve_with_gradients(sc, b.T0, SolveOptions(iterations=20, precision=Precision.SINGLE))
+        job = submit_with_gradients_host(b.basis, b.anchor, b.start, b.end, b.T0, iterations=20,
+                                         chunk=256, depth=2, out=host_buffers(b.size, K))
+        jobs.append((job, res, grads))
+    for job, res, grads in jobs:
+        out = job.wait()
+        for name, dev in (("T", res.T), ("points", res.points), ("length", res.length),
+                          ("status", res.status), ("d_basis", grads.basis), ("d_anchor", grads.anchor),
+                          ("d_start", grads.start), ("d_end", grads.end)):
+            assert np.array_equal(out[name], dev.cpu().numpy()), name
