@@ -82,3 +82,31 @@ def test_mixed_loss_matches_finite_differences():
         ad = t.grad[(slice(None),) + idx].cpu().numpy()
         err = np.abs(ad - fd) / np.maximum(np.abs(fd), 1e-3)
         assert np.all(err[conv] < 1e-4), (k, idx, float(err[conv].max()))
+
+
+def test_implicit_gradient_matches_autodiff_through_iterations():
+    """Independent check of the VJP kernel: autograd through the same BFGS
+    written in torch ops (tools/implicit_vs_ad.py) agrees with the implicit
+    gradient on converged paths (fp64, 50 iterations)."""
+    import importlib.util
+    import os
+
+    spec = importlib.util.spec_from_file_location(
+        "implicit_vs_ad", os.path.join(os.path.dirname(__file__), "..", "tools", "implicit_vs_ad.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    b = datagen.gen_batch(23, datagen.all_orderings(2), 512)
+    xs = [torch.from_numpy(np.ascontiguousarray(x)).to("cuda", torch.float64).requires_grad_(True)
+          for x in (b.basis, b.anchor, b.start, b.end)]
+    _, L = mod.bfgs_torch(*xs, 50)
+    L.sum().backward()
+    res, g = solve_with_gradients(BatchScene(b.basis, b.anchor, b.start, b.end), b.T0,
+                                  SolveOptions(iterations=50, precision=Precision.DOUBLE))
+    conv = (res.status & _lib.STATUS_UNCONVERGED_MASK) == 0
+    fin = torch.isfinite(xs[1].grad.reshape(b.size, -1)).all(1)
+    m = conv & fin
+    assert m.float().mean() > 0.4
+    for ad, im in ((xs[0].grad, g.basis), (xs[1].grad, g.anchor), (xs[2].grad, g.start), (xs[3].grad, g.end)):
+        a, i = ad[m].reshape(int(m.sum()), -1), im[m].reshape(int(m.sum()), -1)
+        rel = torch.linalg.vector_norm(a - i, dim=1) / torch.linalg.vector_norm(i, dim=1)
+        assert float(rel.median()) < 1e-6 and float(torch.quantile(rel, 0.9)) < 1e-3
