@@ -221,3 +221,29 @@ def test_host_submit_chain_equals_device_step():
                           ("status", res.status), ("d_basis", grads.basis), ("d_anchor", grads.anchor),
                           ("d_start", grads.start), ("d_end", grads.end)):
             assert np.array_equal(out[name], dev.cpu().numpy()), name
+
+
+def test_order0_through_every_entry_point():
+    """K = 0 (a straight TX -> RX segment): device, host and submitted calls
+    agree; L = |end - start| and dL/dstart = -dL/dend = -(end - start)/L."""
+    from paper_2510_16172_b200.solver import host_buffers, solve_with_gradients_host, submit_with_gradients_host
+
+    rng = np.random.default_rng(3)
+    B = 1000
+    start = rng.uniform(-10, 10, (B, 3)).astype(np.float32)
+    end = rng.uniform(-10, 10, (B, 3)).astype(np.float32)
+    basis = np.zeros((B, 0, 3, 2), np.float32)
+    anchor = np.zeros((B, 0, 3), np.float32)
+    res, g = solve_with_gradients(BatchScene(basis, anchor, start, end), None,
+                                  SolveOptions(iterations=5, precision=Precision.SINGLE))
+    d = end.astype(np.float64) - start
+    L = np.linalg.norm(d, axis=1)
+    assert np.allclose(res.length.cpu().numpy(), L, rtol=1e-6)
+    assert np.allclose(g.end.cpu().numpy(), d / L[:, None], atol=1e-6)
+    assert np.allclose(g.start.cpu().numpy(), -d / L[:, None], atol=1e-6)
+    out = solve_with_gradients_host(basis, anchor, start, end, iterations=5, out=host_buffers(B, 0))
+    job = submit_with_gradients_host(basis, anchor, start, end, iterations=5, out=host_buffers(B, 0))
+    for o in (out, job.wait()):
+        assert np.array_equal(o["length"], res.length.cpu().numpy())
+        assert np.array_equal(o["d_start"], g.start.cpu().numpy())
+        assert np.array_equal(o["d_end"], g.end.cpu().numpy())
