@@ -580,11 +580,27 @@ struct MinBlocks {
 #ifndef FP_TILE_MIN_BLOCKS_K5
 #define FP_TILE_MIN_BLOCKS_K5 2
 #endif
+// fp64 tile kernels (registers are pairs). Measured on B200 (tools/f64_ab.py,
+// 2^20 paths, fused): uncapped (254 registers at K=3, 2 CTAs/SM) vs capped —
+// K=1 6 CTAs 0.325 -> 0.319 ms, K=2 4 CTAs 0.680 -> 0.534 ms, K=3 3 CTAs
+// 0.881 -> 0.853 ms (the spills stay in L1); K=4/5 uncapped is best.
+#ifndef FP_TILE_MIN_BLOCKS_F64_K1
+#define FP_TILE_MIN_BLOCKS_F64_K1 6
+#endif
+#ifndef FP_TILE_MIN_BLOCKS_F64_K2
+#define FP_TILE_MIN_BLOCKS_F64_K2 4
+#endif
+#ifndef FP_TILE_MIN_BLOCKS_F64_K3
+#define FP_TILE_MIN_BLOCKS_F64_K3 3
+#endif
 template <typename R, int K, unsigned MASK>
 struct LaunchMin {
   static constexpr int value =
       MASK != kAnyMask ? MinBlocks<R, Lay<K, MASK>::NA>::value
-      : sizeof(R) == 8 ? 1  // fp64: registers are pairs; no cap (as the dense fp64 kernels)
+      : sizeof(R) == 8 ? (K == 1   ? FP_TILE_MIN_BLOCKS_F64_K1
+                          : K == 2 ? FP_TILE_MIN_BLOCKS_F64_K2
+                          : K == 3 ? FP_TILE_MIN_BLOCKS_F64_K3
+                                   : 1)
                        : (K == 1   ? FP_TILE_MIN_BLOCKS_K1
                           : K == 2 ? FP_TILE_MIN_BLOCKS_K2
                           : K == 3 ? FP_TILE_MIN_BLOCKS_K3
