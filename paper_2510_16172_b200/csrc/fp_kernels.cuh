@@ -563,7 +563,8 @@ struct MinBlocks {
 
 // Tile kernels (MASK == kAnyMask): one register budget for all variants of
 // the order. Measured on B200: order 1 runs 8 CTAs/SM (64 registers, no
-// spills) and order 2 runs 5 (96 registers) instead of the NA rule's 4;
+// spills), order 2 runs 5 (96 registers), order 5 runs 3 (168 registers;
+// its spills stay in L1) instead of the NA rule;
 // FP_TILE_MIN_BLOCKS_K<k> overrides.
 #ifndef FP_TILE_MIN_BLOCKS_K1
 #define FP_TILE_MIN_BLOCKS_K1 8
@@ -578,7 +579,7 @@ struct MinBlocks {
 #define FP_TILE_MIN_BLOCKS_K4 3
 #endif
 #ifndef FP_TILE_MIN_BLOCKS_K5
-#define FP_TILE_MIN_BLOCKS_K5 2
+#define FP_TILE_MIN_BLOCKS_K5 3  // 2 before the per-op slab layout; 3: fused 2.230 -> 2.066 ms
 #endif
 // fp64 tile kernels (registers are pairs). Measured on B200 (tools/f64_ab.py,
 // 2^20 paths, fused): uncapped (254 registers at K=3, 2 CTAs/SM) vs capped —
