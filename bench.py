@@ -9,8 +9,12 @@ that fused kernel over the batch; inputs (654 MB/step) exceed the 126 MB L2.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Multi-GPU: torchrun, one rank per GPU; each rank owns its own 2^22 paths
-(weak scaling, no data-path collective); time = max over ranks.
+Multi-GPU: one process per GPU. Under torchrun (WORLD_SIZE set) each process
+is one rank; `--gpus N` without torchrun relaunches itself through
+torch.distributed.run with N ranks (127.0.0.1). Each rank owns its own 2^22
+paths (weak scaling, no data-path collective); time = max over ranks.
+`--backend gloo` lets several ranks share one GPU (a functional check of
+the multi-rank path; NCCL needs one device per rank).
 """
 
 from __future__ import annotations
@@ -106,13 +110,44 @@ def _dist():
     return ws, rank, local
 
 
+def _init_dist(args):
+    """Bind this process to its GPU and (N > 1) join the process group.
+
+    NCCL: one device per rank (LOCAL_RANK). gloo: ranks may share devices
+    (LOCAL_RANK modulo the device count) — reductions then stage through
+    host memory."""
+    import torch
+
+    ws, rank, local = _dist()
+    ndev = torch.cuda.device_count()
+    if ws > 1 and args.backend == "nccl" and local >= ndev:
+        raise SystemExit(f"rank {rank}: LOCAL_RANK {local} but only {ndev} GPU(s); NCCL needs one "
+                         "device per rank (use --backend gloo to share devices)")
+    torch.cuda.set_device(local % max(1, ndev) if ws > 1 else 0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    if ws > 1:
+        import torch.distributed as dist
+
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
+    return ws, rank, local, dev
+
+
+def _reduce_dev(dev):
+    import torch.distributed as dist
+
+    return "cpu" if dist.get_backend() == "gloo" else dev
+
+
 def _max_over_ranks(x: float, ws: int, dev) -> float:
     if ws == 1:
         return x
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    t = torch.tensor([x], dtype=torch.float64, device=_reduce_dev(dev))
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -123,9 +158,39 @@ def _sum_over_ranks(x: float, ws: int, dev) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    t = torch.tensor([x], dtype=torch.float64, device=_reduce_dev(dev))
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
+
+
+def _devices_in_use(ws: int, dev) -> int:
+    """Distinct GPUs across the ranks (ranks may share one under gloo)."""
+    if ws == 1:
+        return 1
+    import torch.distributed as dist
+
+    ids = [None] * ws
+    dist.all_gather_object(ids, (os.uname().nodename, dev.index))
+    return len(set(ids))
+
+
+def _self_launch(args, argv) -> int:
+    """`--gpus N` (N > 1) without torchrun: relaunch this script through
+    torch.distributed.run with N ranks on this node, as the driver does."""
+    import socket
+    import subprocess
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    # the communicator's init line reports nranks = N (stderr)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__), *argv]
+    return subprocess.run(cmd, env=env).returncode
 
 
 def _barrier(ws):
@@ -187,6 +252,7 @@ def run_reference(args):
     ws, rank, _ = _dist()
     if rank != 0:
         return 0
+    ws = max(ws, args.gpus)
     from paper_2510_16172_b200 import datagen
     from oracle.cpu_baseline import CpuPool
 
@@ -239,15 +305,7 @@ def run_ours(args):
     from paper_2510_16172_b200 import _lib, datagen
     from paper_2510_16172_b200.batching import BatchScene
 
-    ws, rank, local = _dist()
-    if ws > 1:
-        import torch.distributed as dist
-
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(0)
-    dev = torch.device("cuda", torch.cuda.current_device())
+    ws, rank, local, dev = _init_dist(args)
     lib = _lib.load()
     _lib.set_kernel_policy(args.policy)
     K, I, F = args.order, args.iterations, 1
@@ -282,7 +340,9 @@ def run_ours(args):
             _lib.check(rc, "fp_solve_f32")
 
     gate = torch.zeros(1, dtype=torch.int32).pin_memory()
-    use_gate = K <= _lib.TILE_MAX_ORDER and args.policy in ("auto", "tile")
+    # (never with ranks sharing a device: their gates would wait on other contexts' time slices)
+    use_gate = (K <= _lib.TILE_MAX_ORDER and args.policy in ("auto", "tile") and not args.no_gate
+                and not (ws > 1 and args.backend == "gloo"))
 
     def timed(fn, steps, warmup, sampler=None):
         for _ in range(warmup):
@@ -353,18 +413,23 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         pin = lambda shape, dt=torch.float32: torch.empty(shape, dtype=dt, pin_memory=True)  # noqa: E731
-        hin = [pin(tuple(host.basis.shape)), pin(tuple(host.anchor.shape)), pin((B, 3)), pin((B, 3)),
-               pin((B, K, 2))]
-        for t, a in zip(hin, (host.basis, host.anchor, host.start, host.end, host.T0)):
+        # Inputs: the scene (basis, anchor, TX, RX); the zero T0 is set on the
+        # device (T0 = NULL). Outputs: T*, L*, the scene gradient and status;
+        # the interaction points are not copied back (they follow from T*,
+        # as the reference derives them on the host, bench.py:313-314).
+        assert not host.T0.any()
+        hin = [pin(tuple(host.basis.shape)), pin(tuple(host.anchor.shape)), pin((B, 3)), pin((B, 3))]
+        for t, a in zip(hin, (host.basis, host.anchor, host.start, host.end)):
             t.numpy()[...] = a
-        hout = [pin((B, K, 2)), pin((B, K, 3)), pin((B,)), pin((B, K, 3, 2)), pin((B, K, 3)),
+        hout = [pin((B, K, 2)), None, pin((B,)), pin((B, K, 3, 2)), pin((B, K, 3)),
                 pin((B, 3)), pin((B, 3)), pin((B,), torch.uint8)]
         h2d = sum(t.numel() * t.element_size() for t in hin)
-        d2h = sum(t.numel() * t.element_size() for t in hout)
+        d2h = sum(t.numel() * t.element_size() for t in hout if t is not None)
+        Pn = lambda t: None if t is None else t.data_ptr()  # noqa: E731
 
         def e2e_step():
-            rc = lib.fp_solve_vjp_host_f32(*(P(t) for t in hin), B, K, I, F, 1.0, _lib.VJP_FULL,
-                                           *(P(t) for t in hout), args.chunk, 3)
+            rc = lib.fp_solve_vjp_host_f32(*(P(t) for t in hin), None, B, K, I, F, 1.0, _lib.VJP_FULL,
+                                           *(Pn(t) for t in hout), args.chunk, 3)
             if rc:
                 _lib.check(rc, "fp_solve_vjp_host_f32")
 
@@ -372,14 +437,14 @@ def run_ours(args):
         # submitted before step i is waited for, so its host-to-device copies
         # overlap step i's device-to-host copies (two output sets in flight).
         # Every step still copies its inputs in and its results out.
-        hout2 = [hout, [pin(tuple(t.shape), t.dtype) for t in hout]]
+        hout2 = [hout, [None if t is None else pin(tuple(t.shape), t.dtype) for t in hout]]
         import ctypes
 
         def e2e_submit(i):
             tk = ctypes.c_uint64(0)
-            rc = lib.fp_solve_vjp_host_submit_f32(*(P(t) for t in hin), B, K, I, F, 1.0, _lib.VJP_FULL,
-                                                  *(P(t) for t in hout2[i % 2]), args.stream_chunk, 2,
-                                                  ctypes.addressof(tk))
+            rc = lib.fp_solve_vjp_host_submit_f32(*(P(t) for t in hin), None, B, K, I, F, 1.0,
+                                                  _lib.VJP_FULL, *(Pn(t) for t in hout2[i % 2]),
+                                                  args.stream_chunk, 2, ctypes.addressof(tk))
             if rc:
                 _lib.check(rc, "fp_solve_vjp_host_submit_f32")
             return tk.value
@@ -413,6 +478,9 @@ def run_ours(args):
                         "submitted back to back, each waited one step later; copy-in, compute and "
                         f"copy-out streams over 2 device chunk slots of up to {args.stream_chunk} "
                         "paths)"),
+               "copies": ("in: basis, anchor, start, end (T0 = NULL: zero init on the device); "
+                          "out: T, length, d_basis, d_anchor, d_start, d_end, status (points "
+                          "skipped: derivable from T)"),
                "blocking": {"ms_per_step": e_blocking_s * 1e3,
                             "value": _sum_over_ranks(e_conv, ws, dev) / e_blocking_s,
                             "path": ("fp_solve_vjp_host_f32 (one blocking call per step; chunks of "
@@ -435,10 +503,12 @@ def run_ours(args):
                          "implicit gradient like the reference", "wall_s": w,
                "converged_fraction": c / n}
 
+    n_devices = _devices_in_use(ws, dev)
     if rank == 0:
         clocks = sampler.summary()
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "devices": n_devices,
+            "backend": args.backend if ws > 1 else None, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded numpy PCG64, SURVEY.md §8(d) generator)",
@@ -480,15 +550,7 @@ def run_scene(args):
     from paper_2510_16172_b200.scene import (DeviceScene, blockers, candidate_count, make_urban_scene,
                                              trace, visibility)
 
-    ws, rank, local = _dist()
-    if ws > 1:
-        import torch.distributed as dist
-
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(0)
-    dev = torch.device("cuda", torch.cuda.current_device())
+    ws, rank, local, dev = _init_dist(args)
     _lib.set_kernel_policy(args.policy)
     grad = args.workload == "config4"
     sc = make_urban_scene(seed=0, alphabet=args.alphabet)
@@ -523,6 +585,7 @@ def run_scene(args):
     launches = _lib.launch_count() - n0
     _barrier(ws)
     ms = _max_over_ranks(e0.elapsed_time(e1), ws, dev) / args.steps
+    n_devices = _devices_in_use(ws, dev)
     if rank == 0:
         per_order = [{"order": o.order, "candidates": o.candidates, "converged": o.converged,
                       "in_bounds": o.in_bounds, "valid": o.valid} for o in res.orders]
@@ -531,7 +594,8 @@ def run_scene(args):
                        if not grad else "inverse-design gradient steps/sec (trace + implicit VJP + allreduce)"),
             "value": (total / (ms * 1e-3)) if not grad else 1e3 / ms,
             "unit": "paths/s" if not grad else "steps/s",
-            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "n_gpus": ws, "devices": n_devices, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic city (paper_2510_16172_b200.scene.make_urban_scene, seed 0)",
             "config": {"workload": args.workload, "buildings": 16, "walls": int(sc.walls.shape[0]),
@@ -682,7 +746,14 @@ def main(argv=None):
                          "inside the timed step; default keeps them sharded")
     ap.add_argument("--visibility", action="store_true",
                     help="config3/4: also flag occluded / wrong-side paths (fp_visibility_f64)")
-    args = ap.parse_args(argv)
+    ap.add_argument("--backend", choices=("nccl", "gloo"), default="nccl",
+                    help="process group for N > 1 (gloo: ranks may share one GPU)")
+    ap.add_argument("--no-gate", action="store_true",
+                    help="do not hold the stream behind fp_gate_wait (for runs under ncu)")
+    raw = list(sys.argv[1:] if argv is None else argv)
+    args = ap.parse_args(raw)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        return _self_launch(args, raw)
     if args.workload in ("config3", "config4") and args.impl == "ours":
         return run_scene(args)
     if args.workload == "config1" and args.impl == "ours":

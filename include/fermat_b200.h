@@ -17,8 +17,13 @@
  *   - Every call is asynchronous on `stream` (a cudaStream_t; NULL = legacy
  *     default stream) and returns an fp_error code; kernels never raise —
  *     per-path conditions are reported in a status byte (FP_STATUS_*).
- *   - Optional outputs may be NULL.
- *   - No global state besides a launch counter (fp_launch_count).
+ *   - Optional outputs may be NULL (not computed, not copied).
+ *   - Library state: a launch counter (fp_launch_count), the kernel policy
+ *     (fp_set_kernel_policy), and per-DEVICE caches created on first use on
+ *     the calling thread's current device: the kernels' shared-memory
+ *     attributes, the layout-probe counters of the tile dispatch, the side
+ *     streams of the bucketed dispatch and the host-buffer pipeline. Calls on
+ *     different devices never share any of them.
  */
 #ifndef FERMAT_B200_H
 #define FERMAT_B200_H
@@ -38,9 +43,10 @@ enum fp_error {
   FP_ERR_UNSUPPORTED_MODE = 4
 };
 
-/* Largest interaction count served by the register-resident kernels. The
- * reference allows up to 64 (geometry.py:23); orders above this are rejected. */
-#define FP_MAX_ORDER 64 /* geometry.py:23 MAX_INTERACTIONS; orders 9..64 run the warp-per-path solver */
+/* Largest interaction count: the reference's MAX_INTERACTIONS (geometry.py:23).
+ * Orders 1..8 run the register-resident per-thread kernels, orders 9..64 the
+ * warp-per-path solver (csrc/fp_wide.cu); larger K is FP_ERR_UNSUPPORTED_ORDER. */
+#define FP_MAX_ORDER 64
 
 /* ---- per-path status bits (uint8) --------------------------------------- */
 #define FP_STATUS_DEGENERATE_ENTRY 0x01u /* entry segment <= eps: reference raises DegenerateSegment for the batch (solver.py:166) */
@@ -118,7 +124,12 @@ int fp_solve_vjp_f64(const double* basis, const double* anchor, const double* st
  * out, pipelined over chunks of `chunk` paths: a copy-in, a compute and a
  * copy-out stream over a ring of `depth` (1..8) device chunk slots, so both
  * PCIe directions stay busy; blocks until the outputs are in host memory.
- * Pinned host memory gives full PCIe bandwidth. */
+ * Pinned host memory gives full PCIe bandwidth. basis/anchor (K > 0) and
+ * start/end are required (NULL: FP_ERR_INVALID_ARGUMENT). T0 == NULL means
+ * zero initialisation (set on the device: no host-to-device copy). Every
+ * output may be NULL and is then neither computed into host memory nor
+ * copied: e.g. points_out, which the reference derives on the host from T
+ * (bench.py:313-314 of the reference). */
 int fp_solve_vjp_host_f32(const float* basis, const float* anchor, const float* start,
                           const float* end, const float* T0, int64_t B, int K, int iterations,
                           int fp_iters, float w_L_scale, int mode, float* T_out, float* points_out,

@@ -129,9 +129,14 @@ struct LayoutProbe {
   double frac[kMaxTileOrder + 1] = {};
   int since[kMaxTileOrder + 1] = {};   // tile calls since the last probe
 };
+// One probe per device: its counters, pinned slots and events belong to the
+// device the tile kernels run on, and each device sees its own layouts.
+constexpr int kMaxDevices = 64;
 static LayoutProbe& probe() {
-  static LayoutProbe p;
-  return p;
+  static LayoutProbe p[kMaxDevices];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+  return p[dev];
 }
 
 static bool tile_preferred(int K) {
@@ -265,6 +270,9 @@ static int dispatch(int K, const PathArgs<R>& a, int op, cudaStream_t s, int rou
     for (int m = 0; m < plan.nb; ++m) live += plan.count[m] > 0;
     SideStreams& ss = side_streams();
     const bool fan = live > 1 && g_policy.load() != FP_POLICY_AUTO_SERIAL;
+    // the device's side streams serve one caller at a time, fork through join
+    std::unique_lock<std::mutex> fan_lock(ss.mu, std::defer_lock);
+    if (fan) fan_lock.lock();
     if (e == cudaSuccess && fan) e = ss.fork(s, live);
     int k = 0;
     for (unsigned m = 0; m < unsigned(plan.nb) && e == cudaSuccess; ++m) {
@@ -613,7 +621,10 @@ struct HostPipe {
     return cudaSuccess;
   }
 };
-static HostPipe g_pipe;
+// One pipeline per device (streams, slots and events live on that device);
+// tickets carry the device ordinal in their top byte.
+static HostPipe g_pipes[kMaxDevices];
+constexpr int kTicketShift = 56;
 
 // The copies of one chunk in one direction, one cudaMemcpyAsync per array.
 static cudaError_t copy_arrays(void** dst, void** src, size_t* bytes, size_t n, cudaMemcpyKind kind,
@@ -634,14 +645,21 @@ static int host_submit(const R* basis, const R* anchor, const R* start, const R*
   if (ticket) *ticket = 0;  // 0: nothing in flight
   if (B < 0 || iterations < 1 || fp_iters < 1 || depth < 1 || depth > 8)
     return FP_ERR_INVALID_ARGUMENT;
+  if (mode != FP_VJP_FULL && mode != FP_VJP_ENVELOPE) return FP_ERR_UNSUPPORTED_MODE;
   if (K < 0 || K > FP_MAX_ORDER) return FP_ERR_UNSUPPORTED_ORDER;
   if (B == 0) return FP_OK;
+  // Required inputs (the same contract as the device entries); T0 == NULL
+  // means zero initialisation, done on the device (no host-to-device copy).
+  if (start == nullptr || end == nullptr) return FP_ERR_INVALID_ARGUMENT;
+  if (K > 0 && (basis == nullptr || anchor == nullptr)) return FP_ERR_INVALID_ARGUMENT;
   if (chunk <= 0) chunk = 1 << 18;
   chunk = (chunk + kThreads - 1) / kThreads * kThreads;
-  std::lock_guard<std::mutex> lock(g_pipe.mu);
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_status(e);
+  if (dev < 0 || dev >= kMaxDevices) return FP_ERR_INVALID_ARGUMENT;
+  HostPipe& g_pipe = g_pipes[dev];
+  std::lock_guard<std::mutex> lock(g_pipe.mu);
   // Per slot: inputs then outputs for `chunk` paths, 256-byte aligned pieces.
   const int64_t w_in[5] = {6 * K, 3 * K, 3, 3, 2 * K};
   const int64_t w_out[7] = {2 * K, 3 * K, 1, 6 * K, 3 * K, 3, 3};
@@ -721,6 +739,9 @@ static int host_submit(const R* basis, const R* anchor, const R* start, const R*
         }
         if ((e = copy_arrays(dv, sv, nb, m, cudaMemcpyHostToDevice, s_in)) != cudaSuccess)
           return cuda_status(e);
+        if (T0 == nullptr && K > 0 &&
+            (e = cudaMemsetAsync(din[4], 0, size_t(n * w_in[4]) * sizeof(R), s_in)) != cudaSuccess)
+          return cuda_status(e);
       }
       if ((e = cudaEventRecord(g_pipe.ev_in[j], s_in)) != cudaSuccess) return cuda_status(e);
       // solve + VJP (the output region is free once chunk c - depth was copied out)
@@ -777,13 +798,17 @@ static int host_submit(const R* basis, const R* anchor, const R* start, const R*
     return cuda_status(e);
   }
   if ((e = cudaEventRecord(ev, s_out)) != cudaSuccess) return cuda_status(e);
-  if (ticket) *ticket = t;
+  if (ticket) *ticket = t | (uint64_t(dev) << kTicketShift);
   return FP_OK;
 }
 
 // Wait until the outputs of submitted call `ticket` are in host memory.
-static int host_wait(uint64_t ticket) {
-  if (ticket == 0) return FP_OK;
+static int host_wait(uint64_t ticket_in) {
+  if (ticket_in == 0) return FP_OK;
+  const int dev = int(ticket_in >> kTicketShift);
+  const uint64_t ticket = ticket_in & ((uint64_t(1) << kTicketShift) - 1);
+  if (dev >= kMaxDevices || ticket == 0) return FP_ERR_INVALID_ARGUMENT;
+  HostPipe& g_pipe = g_pipes[dev];
   cudaEvent_t ev = nullptr;
   {
     std::lock_guard<std::mutex> lock(g_pipe.mu);

@@ -220,8 +220,10 @@ template cudaError_t bucket_plan<double>(const double*, int64_t, int, BucketScra
 
 // ---- side streams: overlap the tails of the per-mask launches ----------------
 SideStreams& side_streams() {
-  static SideStreams ss;
-  return ss;
+  static SideStreams ss[64];  // per device: the streams and events belong to it
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+  return ss[dev];
 }
 
 cudaError_t SideStreams::fork(cudaStream_t parent, int n) {

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <mutex>
 
 namespace fp {
 
@@ -41,9 +42,10 @@ struct SideStreams {
   cudaEvent_t start;
   bool ready = false;
   int used = 0;
+  std::mutex mu;  // held by the caller from fork through join
   cudaError_t fork(cudaStream_t parent, int n);
   cudaError_t join(cudaStream_t parent);
 };
-SideStreams& side_streams();
+SideStreams& side_streams();  // the current device's
 
 }  // namespace fp

@@ -10,6 +10,8 @@
 // (bucketed dispatch), threads read and write their records directly.
 #pragma once
 
+#include <atomic>
+
 #include "fp_path.cuh"
 
 namespace fp {
@@ -639,12 +641,18 @@ cudaError_t launch_path_impl(const PathArgs<R>& a, cudaStream_t stream) {
   const int64_t rows = a.rows ? a.n_rows : a.B - a.row_begin;
   if (rows <= 0) return cudaSuccess;
   constexpr size_t smem = smem_bytes<R, K, OP>();
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(path_kernel<R, K, MASK, OP>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  // The dynamic shared-memory attribute is per device: one bit per device
+  // ordinal records that this instantiation was configured there.
+  static std::atomic<uint64_t> configured{0};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(configured.load(std::memory_order_acquire) & bit)) {
+    e = cudaFuncSetAttribute(path_kernel<R, K, MASK, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(smem));
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured.fetch_or(bit, std::memory_order_acq_rel);
   }
   const int64_t blocks = (rows + kThreads - 1) / kThreads;
   path_kernel<R, K, MASK, OP><<<dim3(unsigned(blocks)), dim3(kThreads), smem, stream>>>(a);

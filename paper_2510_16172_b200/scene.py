@@ -258,13 +258,19 @@ def _share(total: int, rank: int, world: int) -> tuple[int, int]:
     return total * rank // world, total * (rank + 1) // world
 
 
+def _host_staged() -> bool:
+    """gloo (the CPU tests, and ranks sharing one GPU) moves CPU tensors only:
+    device tensors are staged through host memory for its collectives."""
+    return torch.distributed.get_backend() == "gloo"
+
+
 def reduce_sum(t: torch.Tensor, world: int) -> torch.Tensor:
     """Sum over ranks (NCCL on GPU tensors, gloo in the CPU tests); identity for one rank."""
     if world <= 1:
         return t
-    out = t.clone()
+    out = t.detach().to("cpu", copy=True) if _host_staged() else t.clone()
     torch.distributed.all_reduce(out)
-    return out
+    return out.to(t.device)
 
 
 def reduce_sum_many(ts, world: int):
@@ -272,7 +278,11 @@ def reduce_sum_many(ts, world: int):
     if world <= 1:
         return list(ts)
     flat = torch.cat([t.reshape(-1) for t in ts])
+    dev = flat.device
+    if _host_staged():
+        flat = flat.cpu()
     torch.distributed.all_reduce(flat)
+    flat = flat.to(dev)
     out, o = [], 0
     for t in ts:
         out.append(flat[o:o + t.numel()].reshape(t.shape))
@@ -288,6 +298,15 @@ def gather_rows(ts, world: int):
     the CPU tests). Identity for one rank."""
     if world <= 1:
         return list(ts)
+    dist = torch.distributed
+    dev = ts[0].device
+    if _host_staged():
+        return [t.to(dev) for t in gather_rows([t.cpu() for t in ts], world)] if dev.type != "cpu" \
+            else _gather_rows(ts, world)
+    return _gather_rows(ts, world)
+
+
+def _gather_rows(ts, world: int):
     dist = torch.distributed
     dev = ts[0].device
     n = torch.tensor([ts[0].shape[0]], dtype=torch.int64, device=dev)

@@ -107,8 +107,9 @@ def solve(scene: BatchScene, T0=None, opts: SolveOptions = SolveOptions(), *,
         points=_empty((B, K, 3), dt, dev) if want_points else None,
         length=_empty((B,), dt, dev),
         status=_empty((B,), torch.uint8, dev),
-        trace_len=_empty((I, B), dt, dev) if opts.record_trace else None,
-        trace_gnorm=_empty((I, B), dt, dev) if opts.record_trace else None,
+        # order 0 runs no iterations: empty per-path traces (solver.py:160-164)
+        trace_len=_empty((I if K else 0, B), dt, dev) if opts.record_trace else None,
+        trace_gnorm=_empty((I if K else 0, B), dt, dev) if opts.record_trace else None,
         H=_empty((B, 2 * K, 2 * K), dt, dev) if return_state else None,
     )
     fn = lib.fp_solve_f32 if dt == torch.float32 else lib.fp_solve_f64
@@ -182,22 +183,29 @@ def _host_call(submit: bool, basis, anchor, start, end, T0, iterations, fixed_po
     anchor = np.ascontiguousarray(anchor, ft)
     start = np.ascontiguousarray(start, ft)
     end = np.ascontiguousarray(end, ft)
-    T0 = np.zeros((B, K, 2), ft) if T0 is None else np.ascontiguousarray(T0, ft)
-    if anchor.shape != (B, K, 3) or start.shape != (B, 3) or end.shape != (B, 3) or T0.shape != (B, K, 2):
+    # T0 = None: zero initialisation on the device (no host-to-device copy)
+    T0 = None if T0 is None else np.ascontiguousarray(T0, ft)
+    if (anchor.shape != (B, K, 3) or start.shape != (B, 3) or end.shape != (B, 3)
+            or (T0 is not None and T0.shape != (B, K, 2))):
         raise ShapeMismatch("host arrays must be basis (B,K,3,2), anchor (B,K,3), start/end (B,3), T0 (B,K,2)")
     if iterations < 1 or fixed_point_iters < 1:
         raise ValueError("iterations and fixed_point_iters must be >= 1")
     out = out if out is not None else host_buffers(B, K, pinned=False, precision=precision)
+    unknown = set(out) - set(HOST_OUTPUTS)
+    if unknown:
+        raise ValueError(f"unknown outputs {sorted(unknown)}; choose from {HOST_OUTPUTS}")
     for k, v in out.items():
         want = np.uint8 if k == "status" else ft
-        if v.dtype != want or not v.flags.c_contiguous:
-            raise ShapeMismatch(f"out[{k!r}] must be a C-contiguous {np.dtype(want).name} array")
-    P = lambda a: a.ctypes.data  # noqa: E731
+        if v.dtype != want or not v.flags.c_contiguous or v.shape != _host_shape(k, B, K):
+            raise ShapeMismatch(f"out[{k!r}] must be a C-contiguous {np.dtype(want).name} array "
+                                f"of shape {_host_shape(k, B, K)}")
+    # outputs absent from `out` are passed as NULL: neither computed nor copied
+    P = lambda a: None if a is None else a.ctypes.data  # noqa: E731
+    O = lambda k: P(out.get(k))  # noqa: E731
     single = precision is Precision.SINGLE
     args = (P(basis), P(anchor), P(start), P(end), P(T0), B, K, iterations, fixed_point_iters,
-            float(weight), _MODES[mode], P(out["T"]), P(out["points"]), P(out["length"]),
-            P(out["d_basis"]), P(out["d_anchor"]), P(out["d_start"]), P(out["d_end"]),
-            P(out["status"]), int(chunk), int(depth))
+            float(weight), _MODES[mode], O("T"), O("points"), O("length"), O("d_basis"),
+            O("d_anchor"), O("d_start"), O("d_end"), O("status"), int(chunk), int(depth))
     if not submit:
         name = "fp_solve_vjp_host_f32" if single else "fp_solve_vjp_host_f64"
         _lib.check(getattr(lib, name)(*args), name)
@@ -223,7 +231,9 @@ def solve_with_gradients_host(basis, anchor, start, end, T0=None, iterations: in
     kernels, never a silent fp32 downcast). Pinned (page-locked) arrays
     transfer fastest: pass `out` from `host_buffers` to reuse pinned outputs.
     Returns a dict of numpy arrays: T, points, length, status, d_basis,
-    d_anchor, d_start, d_end.
+    d_anchor, d_start, d_end (the keys of `out` when given: a missing key is
+    an output that is skipped). T0 = None is zero initialisation, done on
+    the device.
     """
     return _host_call(False, basis, anchor, start, end, T0, iterations, fixed_point_iters, weight,
                       mode, chunk, depth, out, precision)
@@ -245,17 +255,28 @@ def submit_with_gradients_host(basis, anchor, start, end, T0=None, iterations: i
                       mode, chunk, depth, out, precision)
 
 
-def host_buffers(B: int, K: int, pinned: bool = True, precision: Precision = Precision.SINGLE) -> dict:
-    """Output arrays for solve_with_gradients_host (page-locked when pinned)."""
+HOST_OUTPUTS = ("T", "points", "length", "status", "d_basis", "d_anchor", "d_start", "d_end")
+
+
+def _host_shape(name: str, B: int, K: int) -> tuple:
+    return {"T": (B, K, 2), "points": (B, K, 3), "length": (B,), "status": (B,),
+            "d_basis": (B, K, 3, 2), "d_anchor": (B, K, 3), "d_start": (B, 3), "d_end": (B, 3)}[name]
+
+
+def host_buffers(B: int, K: int, pinned: bool = True, precision: Precision = Precision.SINGLE,
+                 outputs=HOST_OUTPUTS) -> dict:
+    """Output arrays for solve_with_gradients_host (page-locked when pinned).
+
+    `outputs` selects which results the call returns; the others are not
+    computed into host memory and cost no device-to-host copy (e.g. leave
+    out "points", which the reference derives on the host from T).
+    """
     def mk(shape, dt):
         if pinned:
             return torch.empty(shape, dtype=dt, pin_memory=True).numpy()
         return np.empty(shape, dtype=torch.empty(0, dtype=dt).numpy().dtype)
     f = torch.float32 if precision is Precision.SINGLE else torch.float64
-    u8 = torch.uint8
-    return {"T": mk((B, K, 2), f), "points": mk((B, K, 3), f), "length": mk((B,), f),
-            "status": mk((B,), u8), "d_basis": mk((B, K, 3, 2), f), "d_anchor": mk((B, K, 3), f),
-            "d_start": mk((B, 3), f), "d_end": mk((B, 3), f)}
+    return {k: mk(_host_shape(k, B, K), torch.uint8 if k == "status" else f) for k in outputs}
 
 
 def init_params_batch(scene: BatchScene) -> torch.Tensor:

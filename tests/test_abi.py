@@ -65,6 +65,17 @@ def test_host_entry_precision_follows_the_arrays():
         assert fn(*([null] * 5), -1, K, 20, 1, 1.0, 0, *([null] * 8), 0, 3) == 1
         assert fn(*([null] * 5), B, K, 20, 1, 1.0, 0, *([null] * 8), 0, 9) == 1  # depth > 8
         assert fn(*([null] * 5), 0, K, 20, 1, 1.0, 0, *([null] * 8), 0, 3) == 0  # empty batch
+        # a NULL required input is rejected before any copy or launch (T0 may
+        # be NULL: zero initialisation)
+        assert fn(*([null] * 5), B, K, 20, 1, 1.0, 0, *([null] * 8), 0, 3) == 1
+        buf = np.zeros(64)
+        p = buf.ctypes.data
+        for missing in range(4):
+            ins = [p] * 4
+            ins[missing] = null
+            assert fn(*ins, null, B, K, 20, 1, 1.0, 0, *([null] * 8), 0, 3) == 1, missing
+        assert fn(null, null, p, p, null, B, 0, 20, 1, 1.0, 0, *([null] * 8), 0, 9) == 1  # K = 0, depth
+        assert fn(p, p, p, p, null, B, K, 20, 1, 1.0, 7, *([null] * 8), 0, 3) == 4  # bad mode
 
 
 def test_enumerate_candidates_argument_checks():
@@ -87,3 +98,22 @@ def test_host_submit_and_wait_argument_checks():
                                             null) == 1
     assert lib.fp_host_wait(0) == 0
     assert lib.fp_host_wait(1 << 40) == 1  # never issued
+    assert lib.fp_host_wait(70 << 56 | 1) == 1  # no such device
+
+
+def test_host_outputs_are_selectable():
+    """host_buffers(outputs=...) allocates only the chosen results; the
+    others are passed as NULL (neither computed into host memory nor copied)."""
+    from paper_2510_16172_b200 import ShapeMismatch
+    from paper_2510_16172_b200.solver import HOST_OUTPUTS, host_buffers, solve_with_gradients_host
+
+    out = host_buffers(8, 3, pinned=False, outputs=("T", "length", "status"))
+    assert sorted(out) == ["T", "length", "status"]
+    assert set(host_buffers(8, 3, pinned=False)) == set(HOST_OUTPUTS)
+    f4 = np.zeros
+    args = (f4((8, 3, 3, 2), np.float32), f4((8, 3, 3), np.float32), f4((8, 3), np.float32),
+            f4((8, 3), np.float32))
+    with pytest.raises(ValueError):
+        solve_with_gradients_host(*args, out={"bogus": np.zeros(8, np.float32)})
+    with pytest.raises(ShapeMismatch):
+        solve_with_gradients_host(*args, out={"T": np.zeros((8, 3, 3), np.float32)})

@@ -201,6 +201,27 @@ def test_host_pipeline_fp64_equals_device_step(K, chunk):
             assert np.array_equal(out[name], dev.cpu().numpy()), (name, pinned)
 
 
+def test_host_null_T0_and_output_subset():
+    """T0 = NULL is zero initialisation on the device (bitwise the zero-T0
+    call); outputs left out of `out` are skipped, the rest keep their bits."""
+    from paper_2510_16172_b200.solver import host_buffers, solve_with_gradients_host, submit_with_gradients_host
+
+    K = 3
+    b = datagen.gen_batch(91, datagen.all_orderings(K), 333)  # ragged vs the chunk
+    assert not b.T0.any()
+    full = solve_with_gradients_host(b.basis, b.anchor, b.start, b.end, b.T0, iterations=20,
+                                     chunk=512, out=host_buffers(b.size, K))
+    sub = ("T", "length", "status", "d_basis", "d_anchor", "d_start", "d_end")
+    for out in (solve_with_gradients_host(b.basis, b.anchor, b.start, b.end, None, iterations=20,
+                                          chunk=512, out=host_buffers(b.size, K, outputs=sub)),
+                submit_with_gradients_host(b.basis, b.anchor, b.start, b.end, None, iterations=20,
+                                           chunk=512, depth=2,
+                                           out=host_buffers(b.size, K, outputs=sub)).wait()):
+        assert sorted(out) == sorted(sub)
+        for name in sub:
+            assert np.array_equal(out[name], full[name]), name
+
+
 def test_host_submit_chain_equals_device_step():
     """Submitted host-buffer steps chain through one slot ring: several in
     flight (step i + 1's copies overlap step i's), a change of order in
