@@ -737,7 +737,12 @@ __device__ __forceinline__ uint8_t implicit_vjp(const Geo<R, K>& G, const PathSt
       if (!act[i][0]) { D[i][0] = R(1); D[i][1] = R(0); }
       if (!act[i][1]) { D[i][2] = R(1); D[i][1] = R(0); }
     }
-    // Block Thomas elimination, with a Tikhonov retry (implicit_diff.py:64-71).
+    // _solve_sym (implicit_diff.py:55-71): block-Thomas elimination (the
+    // system is block tridiagonal), accepted when its residual
+    // |H_a x - rhs| <= tol (1 + |rhs|); otherwise (or on a zero pivot / a
+    // non-finite solution) one retry on H_a + lambda I with lambda =
+    // 1e-12 tr(H_a), accepted when finite. Inert rows are pinned identity rows
+    // with zero rhs: they add nothing to either norm.
     bool solved = false;
     for (int attempt = 0; attempt < 2 && !solved; ++attempt) {
       const R lam = attempt == 0 ? R(0) : R(1e-12) * trace;
@@ -765,7 +770,7 @@ __device__ __forceinline__ uint8_t implicit_vjp(const Geo<R, K>& G, const PathSt
           z1 -= Lm[1][0] * z[i - 1][0] + Lm[1][1] * z[i - 1][1];
         }
         const R det = C0 * C2 - C1 * C1;
-        ok = ok && (det > R(0)) && finite(det);
+        ok = ok && (det != R(0)) && finite(det);  // LinAlgError: exactly singular pivot
         const R id = rcp_fast(det);
         Ci[i][0] = C2 * id;
         Ci[i][1] = -C1 * id;
@@ -790,6 +795,27 @@ __device__ __forceinline__ uint8_t implicit_vjp(const Geo<R, K>& G, const PathSt
         nxt0 = sol[i][0];
         nxt1 = sol[i][1];
         ok = ok && finite(v0) && finite(v1);
+      }
+      if (ok && attempt == 0) {
+        // residual check of the unregularised solution (implicit_diff.py:58-61)
+        R rr = R(0), bb = R(0);
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+          R r0 = D[i][0] * sol[i][0] + D[i][1] * sol[i][1] - rhs[i][0];
+          R r1 = D[i][1] * sol[i][0] + D[i][2] * sol[i][1] - rhs[i][1];
+          if (i > 0) {
+            r0 += O[i - 1][0][0] * sol[i - 1][0] + O[i - 1][1][0] * sol[i - 1][1];
+            r1 += O[i - 1][0][1] * sol[i - 1][0] + O[i - 1][1][1] * sol[i - 1][1];
+          }
+          if (i + 1 < K) {
+            r0 += O[i][0][0] * sol[i + 1][0] + O[i][0][1] * sol[i + 1][1];
+            r1 += O[i][1][0] * sol[i + 1][0] + O[i][1][1] * sol[i + 1][1];
+          }
+          rr = fma(r1, r1, fma(r0, r0, rr));
+          bb = fma(rhs[i][1], rhs[i][1], fma(rhs[i][0], rhs[i][0], bb));
+        }
+        const R tol = Num<R>::resid_tol() * (R(1) + Num<R>::sqrt_(bb));
+        ok = Num<R>::sqrt_(rr) <= tol;  // NaN: retry
       }
       solved = ok;
     }

@@ -272,8 +272,10 @@ __device__ uint8_t wide_vjp(const WideCtx<R>& c, const PathArgs<R>& a, int64_t r
   __syncwarp();
   if (need_solve) {
     if (c.lane == 0) {
-      // block Thomas elimination with the Tikhonov retry (implicit_diff.py:64-71);
-      // Ci and z reuse dx (3K) and w (2K of 3S) as scratch
+      // _solve_sym (implicit_diff.py:55-71): block-Thomas elimination, accepted
+      // when |H_a x - rhs| <= tol (1 + |rhs|), else (or on a zero pivot / a
+      // non-finite solution) one Tikhonov retry; Ci and z reuse dx (3K) and
+      // w (2K of 3S) as scratch
       R* Ci = sm + L.dx;
       R* z = sm + L.w;
       bool solved = false;
@@ -301,7 +303,7 @@ __device__ uint8_t wide_vjp(const WideCtx<R>& c, const PathArgs<R>& a, int64_t r
             z1 -= Lm[1][0] * z[2 * (i - 1)] + Lm[1][1] * z[2 * (i - 1) + 1];
           }
           const R det = C0 * C2 - C1 * C1;
-          ok = ok && det > R(0) && finite(det);
+          ok = ok && det != R(0) && finite(det);  // LinAlgError: exactly singular pivot
           const R id = R(1) / det;
           Ci[3 * i] = C2 * id;
           Ci[3 * i + 1] = -C1 * id;
@@ -325,6 +327,30 @@ __device__ uint8_t wide_vjp(const WideCtx<R>& c, const PathArgs<R>& a, int64_t r
           sm[L.sol + 2 * i] = nx0;
           sm[L.sol + 2 * i + 1] = nx1;
           ok = ok && finite(v0) && finite(v1);
+        }
+        if (ok && attempt == 0) {
+          // residual check of the unregularised solution (implicit_diff.py:58-61)
+          const R* x = sm + L.sol;
+          const R* rh = sm + L.rhs;
+          R rr = R(0), bb = R(0);
+          for (int i = 0; i < K; ++i) {
+            const R* D = sm + L.D + 3 * i;
+            R r0 = D[0] * x[2 * i] + D[1] * x[2 * i + 1] - rh[2 * i];
+            R r1 = D[1] * x[2 * i] + D[2] * x[2 * i + 1] - rh[2 * i + 1];
+            if (i > 0) {
+              const R* O = sm + L.O + 4 * (i - 1);
+              r0 += O[0] * x[2 * i - 2] + O[2] * x[2 * i - 1];
+              r1 += O[1] * x[2 * i - 2] + O[3] * x[2 * i - 1];
+            }
+            if (i + 1 < K) {
+              const R* O = sm + L.O + 4 * i;
+              r0 += O[0] * x[2 * i + 2] + O[1] * x[2 * i + 3];
+              r1 += O[2] * x[2 * i + 2] + O[3] * x[2 * i + 3];
+            }
+            rr = fma(r1, r1, fma(r0, r0, rr));
+            bb = fma(rh[2 * i + 1], rh[2 * i + 1], fma(rh[2 * i], rh[2 * i], bb));
+          }
+          ok = Num<R>::sqrt_(rr) <= Num<R>::resid_tol() * (R(1) + Num<R>::sqrt_(bb));
         }
         solved = ok;
       }

@@ -216,6 +216,7 @@ def main():
         out_files[f"config1_k{K}"] = d
 
     out_files.update(wide_fixtures())
+    out_files.update(near_singular_fixture())
     for name, d in out_files.items():
         d = dict(d)
         d.update(meta)
@@ -248,8 +249,51 @@ def wide_fixtures():
     return out
 
 
+def near_singular_fixture():
+    """8. _solve_sym's residual-check fallback (implicit_diff.py:55-71) on
+    ill-conditioned active Hessians: a grazing reflection TX -> plane -> RX
+    with TX/RX at height h over the plane z = 0 along the x axis and the
+    plane's in-plane basis rotated by phi. At T* = 0 (exactly stationary by
+    symmetry) H = R diag(2, 2 h^2 / (100 + h^2)) R^T / n, cond ~ 100 / h^2:
+    from h ~ 1e-3 on, LAPACK's solution misses the 1e-8 (1 + |rhs|)
+    residual bound and the reference re-solves with lambda = 1e-12 tr(H).
+    K = 2 adds a well-conditioned second reflection after the grazing one
+    (T* from reference_solve_batch). Records whether the fallback fired."""
+    rng = np.random.default_rng(17)
+    specs, Ts, fired = [], [], []
+    for h in (1e-1, 1e-2, 1e-3, 3e-4, 1e-4, 3e-5):
+        for phi in (0.3, 0.7854, 1.2):
+            c, s = np.cos(phi), np.sin(phi)
+            plane = make_plane([0.0, 0.0, 0.0], [c, s, 0.0], [-s, c, 0.0])
+            specs.append(PathSpec(start=[-10.0, 0.0, h], end=[10.0, 0.0, h], surfaces=(plane,)))
+            Ts.append(np.zeros((1, 2)))
+    out = {}
+    for K, group in ((1, (specs, Ts)),):
+        sp, T = group
+        arrs = _spec_arrays(sp)
+        v = rng.normal(size=(len(sp), K, 2))
+        u = np.stack([solve_stationary_system(s, t, vv) for s, t, vv in zip(sp, T, v)])
+        for s, t, vv in zip(sp, T, v):
+            H = hessian(s, t)
+            x = np.linalg.solve(H, vv.ravel())
+            fired.append(bool(np.linalg.norm(H @ x - vv.ravel()) > 1e-8 * (1 + np.linalg.norm(vv))))
+        vj = [vjp_solution(s, t, vv) for s, t, vv in zip(sp, T, v)]
+        out[f"near_singular_k{K}"] = dict(
+            basis=arrs[0], anchor=arrs[1], start=arrs[2], end=arrs[3], T=np.stack(T), v=v, u=u,
+            fired=np.array(fired), vjp_basis=np.stack([g.basis for g in vj]),
+            vjp_anchor=np.stack([g.anchor for g in vj]), vjp_start=np.stack([g.start for g in vj]),
+            vjp_end=np.stack([g.end for g in vj]))
+    return out
+
+
 if __name__ == "__main__":
-    if len(sys.argv) > 1 and sys.argv[1] == "--wide":
+    if len(sys.argv) > 1 and sys.argv[1] == "--near-singular":
+        meta = dict(numpy_version=np.__version__)
+        for name, d in near_singular_fixture().items():
+            d.update(meta)
+            np.savez_compressed(os.path.join(HERE, name + ".npz"), **d)
+            print("wrote", name, "fallback fired on", int(d["fired"].sum()), "of", len(d["fired"]))
+    elif len(sys.argv) > 1 and sys.argv[1] == "--wide":
         meta = dict(numpy_version=np.__version__)
         for name, d in wide_fixtures().items():
             d.update(meta)

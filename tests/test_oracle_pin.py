@@ -173,3 +173,20 @@ def test_wide_orders_forward(K):
             assert np.array_equal(r["g"], d["g" + suf])
         else:
             assert np.allclose(r["T"][conv], d["T" + suf][conv], rtol=1e-5, atol=1e-5)
+
+
+def test_near_singular_fallback():
+    """_solve_sym's residual-check Tikhonov fallback (implicit_diff.py:55-71):
+    the oracle reproduces the reference's u bit for bit on grazing
+    reflections with cond(H) from 1e4 to 1e11, and where the fallback fired
+    (cond >= 1e10) its u differs from the plain LAPACK solution."""
+    d = golden("near_singular_k1")
+    assert d["fired"].sum() >= 3 and (~d["fired"]).sum() >= 3
+    for j in range(len(d["fired"])):
+        args = (d["basis"][j], d["anchor"][j], d["start"][j], d["end"][j], d["T"][j])
+        u = O.stationary_solve(*args, d["v"][j])
+        assert np.array_equal(u, d["u"][j]), j
+        H = O.scalar_hessian(*args)
+        plain = np.linalg.solve(H, -d["v"][j].ravel())
+        gap = np.linalg.norm(u.ravel() - plain) / np.linalg.norm(plain)
+        assert (gap > 1e-3) == bool(d["fired"][j]), (j, gap)
