@@ -248,7 +248,11 @@ def cpu_sample(batch, n: int):
 
 
 def run_reference(args):
-    """--impl reference: the CPU restatement of the reference path on all host cores."""
+    """--impl reference: the reference's own CPU implementation of the path on all
+    host cores — the genuine package installed into oracle/_ref by
+    oracle/build_ref.py (kind "reference"), else the bit-exact numpy port
+    (kind "port"). With the reference available, the port runs the last
+    step's sample once more as a cross-check (same converged count)."""
     ws, rank, _ = _dist()
     if rank != 0:
         return 0
@@ -258,7 +262,7 @@ def run_reference(args):
 
     K, I = args.order, args.iterations
     batch = datagen.config2(K, 1 << 12 if args.quick else args.sample)
-    pool = CpuPool()
+    pool = CpuPool(kind="auto")
     # Warm-up steps on a small slice also calibrate the per-step sample: the
     # timed steps together stay within ~150 s of CPU work whatever --steps is.
     (b, a, s0, s1, T0), n_cal, _ = cpu_sample(batch, min(batch.size, 8192))
@@ -275,16 +279,28 @@ def run_reference(args):
         wall_total += w
     pool.close()
     value = conv_total / wall_total
+    cross = None
+    if pool.kind == "reference":
+        port = CpuPool(kind="port")
+        pc, pw = port.run(b, a, s0, s1, T0, I)
+        port.close()
+        cross = {"kind": "port", "value": pc / pw, "converged": pc,
+                 "reference_converged": c, "equal": pc == c,
+                 "note": "oracle/fermat_oracle.py on the last step's sample"}
+    what = ("the reference package itself (oracle/_ref, pip-installed from /root/reference by "
+            "oracle/build_ref.py): _bfgs_kernel batched, then per path length_param_gradient + "
+            "vjp_solution(gradient)" if pool.kind == "reference" else
+            "oracle/fermat_oracle.py numpy restatement, batched forward + per-path implicit "
+            "gradient like the reference")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall_total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded numpy PCG64, SURVEY.md §8(d) generator)",
         "config": _config(K, I, args.paths, ws),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": pool.cores, "kind": "port",
-                         "sample": f"{n} paths per step (all 8 orderings equally) of config 2 K={K}; "
-                                   "oracle/fermat_oracle.py numpy restatement, batched forward + "
-                                   "per-path implicit gradient like the reference"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": pool.cores, "kind": pool.kind,
+                         "sample": f"{n} paths per step (all {2 ** K} orderings equally) of config 2 "
+                                   f"K={K}; {what}", "cross_check": cross},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "converged_fraction": conv_total / (n * args.steps),
     }
@@ -335,7 +351,7 @@ def run_ours(args):
 
     def fwd_step():
         rc = lib.fp_solve_f32(P(sc.basis), P(sc.anchor), P(sc.start), P(sc.end), P(T0), B, K, I, F,
-                              P(outT), None, P(outP), P(outL), P(st), None, None, None, stream)
+                              P(outT), None, P(outP), P(outL), P(st), None, None, None, None, stream)
         if rc:
             _lib.check(rc, "fp_solve_f32")
 
@@ -492,16 +508,18 @@ def run_ours(args):
         from oracle.cpu_baseline import CpuPool
 
         (b, a, s0, s1, T0h), n, _ = cpu_sample(host, 1 << 12 if args.quick else args.sample)
-        pool = CpuPool()
+        pool = CpuPool(kind="auto")
         pool.run(b[:pool.cores * 8], a[:pool.cores * 8], s0[:pool.cores * 8], s1[:pool.cores * 8],
                  T0h[:pool.cores * 8], I)  # warm the workers
         c, w = pool.run(b, a, s0, s1, T0h, I)
         pool.close()
-        cpu = {"value": c / w, "unit": UNIT, "cores": pool.cores, "kind": "port",
-               "sample": f"{n} paths (all 8 orderings equally) of this workload; numpy "
-                         "restatement (oracle/fermat_oracle.py): batched forward + per-path "
-                         "implicit gradient like the reference", "wall_s": w,
-               "converged_fraction": c / n}
+        what = ("the reference package (oracle/_ref): _bfgs_kernel batched + per-path "
+                "length_param_gradient + vjp_solution(gradient)" if pool.kind == "reference" else
+                "numpy restatement (oracle/fermat_oracle.py): batched forward + per-path "
+                "implicit gradient like the reference")
+        cpu = {"value": c / w, "unit": UNIT, "cores": pool.cores, "kind": pool.kind,
+               "sample": f"{n} paths (all {2 ** K} orderings equally) of this workload; {what}",
+               "wall_s": w, "converged_fraction": c / n}
 
     n_devices = _devices_in_use(ws, dev)
     if rank == 0:

@@ -61,6 +61,15 @@ enum fp_error {
 #define FP_STATUS_UNCONVERGED_MASK \
   (FP_STATUS_DEGENERATE_ENTRY | FP_STATUS_NOT_STATIONARY | FP_STATUS_NONFINITE | FP_STATUS_DEGENERATE_FINAL)
 
+/* ---- per-iteration BFGS update fate bits (trace_fate, uint8) --------------
+ * The reference's guard rails (solver.py:180-199), recorded with the trace:
+ * 0 = the inverse-Hessian update was applied. */
+#define FP_FATE_CURVATURE_SKIP 0x01u  /* s.y <= 1e-12 |s| |y|: update skipped (solver.py:182-184) */
+#define FP_FATE_NONFINITE_SKIP 0x02u  /* H' not finite: update skipped (solver.py:196-199) */
+#define FP_FATE_ZERO_DIRECTION 0x04u  /* the step-size search met a zero direction (alpha kept) */
+#define FP_FATE_ENTRY_CHECK    0x08u  /* (diagnostic) the magnitude bound on H' was inconclusive and
+                                         every entry was checked for finiteness (fp_path.cuh) */
+
 /* ---- VJP modes ---------------------------------------------------------- */
 enum fp_vjp_mode {
   /* w_L * (dL/dtheta + vjp_solution(grad_T L)) + vjp_solution(v_T):
@@ -79,17 +88,18 @@ enum fp_vjp_mode {
  * Fixed-iteration batch BFGS with the paper's fixed-point step size.
  * T0 (B,K,2) in; T_out/g_out (B,K,2), points_out (B,K,3), length_out (B),
  * status_out (B), trace_len/trace_gnorm (iterations, B) [record_trace],
+ * trace_fate (iterations, B) FP_FATE_* bits [with the trace; NULL = none],
  * H_out (B,2K,2K) [return_state]. */
 int fp_solve_f32(const float* basis, const float* anchor, const float* start, const float* end,
                  const float* T0, int64_t B, int K, int iterations, int fp_iters,
                  float* T_out, float* g_out, float* points_out, float* length_out,
-                 uint8_t* status_out, float* trace_len, float* trace_gnorm, float* H_out,
-                 void* stream);
+                 uint8_t* status_out, float* trace_len, float* trace_gnorm, uint8_t* trace_fate,
+                 float* H_out, void* stream);
 int fp_solve_f64(const double* basis, const double* anchor, const double* start, const double* end,
                  const double* T0, int64_t B, int K, int iterations, int fp_iters,
                  double* T_out, double* g_out, double* points_out, double* length_out,
-                 uint8_t* status_out, double* trace_len, double* trace_gnorm, double* H_out,
-                 void* stream);
+                 uint8_t* status_out, double* trace_len, double* trace_gnorm, uint8_t* trace_fate,
+                 double* H_out, void* stream);
 
 /* ---- implicit-gradient VJP: implicit_diff.vjp_solution / grad_length_wrt_params
  * (implicit_diff.py:39-106 over objective.py:48-135), batched.

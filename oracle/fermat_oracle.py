@@ -110,7 +110,12 @@ def bfgs(basis, anchor, start, end, T0, iterations, fp_iters=1, dtype=np.float32
          trace=False, return_H=False):
     """Fixed-iteration batch BFGS (solver.py:146-215).
 
-    Returns a dict with T, g, and optionally trace_len/trace_gnorm (I,B) and H.
+    Returns a dict with T, g, and optionally trace_len/trace_gnorm (I,B), H,
+    and (with trace) the fate of every update, trace_fate (I,B) uint8: bit 0
+    the curvature test failed (solver.py:182-184), bit 1 H' was not finite
+    and the update was skipped (solver.py:196-199), bit 2 the step size met
+    a zero direction (solver.py:100,110-111). Not a reference output: the
+    reference computes the same masks internally.
     Raises OracleDegenerate when any entry segment is degenerate, like the
     reference's whole-batch DegenerateSegment (solver.py:166).
     """
@@ -131,11 +136,11 @@ def bfgs(basis, anchor, start, end, T0, iterations, fp_iters=1, dtype=np.float32
     H = np.broadcast_to(np.eye(m, dtype=dtype), (B, m, m)).copy()
     g = grad_batch(basis, anchor, start, end, T, eps).reshape(B, m)
     tol = dtype(CURVATURE_TOL)
-    tl, tg = [], []
+    tl, tg, tf = [], [], []
     for _ in range(iterations):
         p = -np.einsum("bij,bj->bi", H, g)
         s, _ = clamped(basis, anchor, start, end, T, eps)
-        alpha, _ = fixed_point_step(basis, s, p.reshape(B, K, 2), fp_iters, eps)
+        alpha, zero = fixed_point_step(basis, s, p.reshape(B, K, 2), fp_iters, eps)
         sigma = alpha[:, None] * p
         T = T + sigma.reshape(B, K, 2)
         g1 = grad_batch(basis, anchor, start, end, T, eps).reshape(B, m)
@@ -152,15 +157,18 @@ def bfgs(basis, anchor, start, end, T0, iterations, fp_iters=1, dtype=np.float32
             outer = np.einsum("bi,bj->bij", sigma, sigma)
             Hn = (H - rho[:, None, None] * (cross + np.swapaxes(cross, 1, 2))
                   + (rho * rho * yHy + rho)[:, None, None] * outer)
+        curv = ok
         ok = ok & np.all(np.isfinite(Hn), axis=(1, 2))
         H = np.where(ok[:, None, None], Hn, H)
         g = g1
         if trace:
             tl.append(length_batch(basis, anchor, start, end, T))
             tg.append(np.sqrt(np.einsum("bi,bi->b", g, g)))
+            tf.append(np.where(curv, 0, 1).astype(np.uint8) | np.where(curv & ~ok, 2, 0).astype(np.uint8)
+                      | np.where(zero, 4, 0).astype(np.uint8))
     out.update(T=T, g=g.reshape(B, K, 2))
     if trace:
-        out.update(trace_len=np.stack(tl), trace_gnorm=np.stack(tg))
+        out.update(trace_len=np.stack(tl), trace_gnorm=np.stack(tg), trace_fate=np.stack(tf))
     if return_H:
         out["H"] = H
     return out

@@ -38,6 +38,11 @@ VIS_WRONG_SIDE = 0x02
 STATUS_UNCONVERGED_MASK = (STATUS_DEGENERATE_ENTRY | STATUS_NOT_STATIONARY
                            | STATUS_NONFINITE | STATUS_DEGENERATE_FINAL)
 
+FATE_CURVATURE_SKIP = 0x01  # trace_fate bits (per BFGS iteration)
+FATE_NONFINITE_SKIP = 0x02
+FATE_ZERO_DIRECTION = 0x04
+FATE_ENTRY_CHECK = 0x08  # diagnostic: the H' magnitude bound was inconclusive, every entry checked
+
 VJP_FULL = 0
 VJP_ENVELOPE = 1
 VJP_MIXED = 2
@@ -58,8 +63,8 @@ _F = C.c_float
 _D = C.c_double
 
 _SIGS = {
-    "fp_solve_f32": [_P] * 5 + [_I64, _I, _I, _I] + [_P] * 8 + [_P],
-    "fp_solve_f64": [_P] * 5 + [_I64, _I, _I, _I] + [_P] * 8 + [_P],
+    "fp_solve_f32": [_P] * 5 + [_I64, _I, _I, _I] + [_P] * 9 + [_P],
+    "fp_solve_f64": [_P] * 5 + [_I64, _I, _I, _I] + [_P] * 9 + [_P],
     "fp_vjp_f32": [_P] * 7 + [_F, _I, _I64, _I] + [_P] * 6 + [_P],
     "fp_vjp_f64": [_P] * 7 + [_D, _I, _I64, _I] + [_P] * 6 + [_P],
     "fp_solve_vjp_f32": [_P] * 5 + [_I64, _I, _I, _I, _P, _F, _I] + [_P] * 8 + [_P],

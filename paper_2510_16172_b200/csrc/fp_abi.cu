@@ -314,10 +314,11 @@ template <typename R>
 static int solve_impl(const R* basis, const R* anchor, const R* start, const R* end, const R* T0,
                       int64_t B, int K, int iterations, int fp_iters, R* T_out, R* g_out,
                       R* points_out, R* length_out, uint8_t* status_out, R* trace_len,
-                      R* trace_gnorm, R* H_out, void* stream) {
+                      R* trace_gnorm, uint8_t* trace_fate, R* H_out, void* stream) {
   if (B < 0 || iterations < 1 || fp_iters < 1) return FP_ERR_INVALID_ARGUMENT;
   if (K < 0 || K > FP_MAX_ORDER) return FP_ERR_UNSUPPORTED_ORDER;
   if ((trace_len == nullptr) != (trace_gnorm == nullptr)) return FP_ERR_INVALID_ARGUMENT;
+  if (trace_fate != nullptr && trace_len == nullptr) return FP_ERR_INVALID_ARGUMENT;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (K == 0) {
     if (B > 0 && (start == nullptr || end == nullptr)) return FP_ERR_INVALID_ARGUMENT;
@@ -329,6 +330,7 @@ static int solve_impl(const R* basis, const R* anchor, const R* start, const R* 
   a.B = B; a.iterations = iterations; a.fp_iters = fp_iters;
   a.T_out = T_out; a.g_out = g_out; a.points_out = points_out; a.length_out = length_out;
   a.status_out = status_out; a.trace_len = trace_len; a.trace_gnorm = trace_gnorm; a.H_out = H_out;
+  a.trace_fate = trace_fate;
   finish_args(a);
   return dispatch<R>(K, a, OP_SOLVE, s);
 }
@@ -828,17 +830,21 @@ extern "C" {
 int fp_solve_f32(const float* basis, const float* anchor, const float* start, const float* end,
                  const float* T0, int64_t B, int K, int iterations, int fp_iters, float* T_out,
                  float* g_out, float* points_out, float* length_out, uint8_t* status_out,
-                 float* trace_len, float* trace_gnorm, float* H_out, void* stream) {
+                 float* trace_len, float* trace_gnorm, uint8_t* trace_fate, float* H_out,
+                 void* stream) {
   return solve_impl<float>(basis, anchor, start, end, T0, B, K, iterations, fp_iters, T_out, g_out,
-                           points_out, length_out, status_out, trace_len, trace_gnorm, H_out, stream);
+                           points_out, length_out, status_out, trace_len, trace_gnorm, trace_fate,
+                           H_out, stream);
 }
 
 int fp_solve_f64(const double* basis, const double* anchor, const double* start, const double* end,
                  const double* T0, int64_t B, int K, int iterations, int fp_iters, double* T_out,
                  double* g_out, double* points_out, double* length_out, uint8_t* status_out,
-                 double* trace_len, double* trace_gnorm, double* H_out, void* stream) {
+                 double* trace_len, double* trace_gnorm, uint8_t* trace_fate, double* H_out,
+                 void* stream) {
   return solve_impl<double>(basis, anchor, start, end, T0, B, K, iterations, fp_iters, T_out, g_out,
-                            points_out, length_out, status_out, trace_len, trace_gnorm, H_out, stream);
+                            points_out, length_out, status_out, trace_len, trace_gnorm, trace_fate,
+                            H_out, stream);
 }
 
 int fp_vjp_f32(const float* basis, const float* anchor, const float* start, const float* end,

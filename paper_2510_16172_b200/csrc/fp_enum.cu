@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(kThreads, (MinBlocks<float, Lay<K, MASK>::NA>:
       G.nz = a.nz;
       P.zero_t();
       P.eval(G, P.g);
-      uint8_t st = bfgs_solve<float, K, MASK>(G, P, a.iterations, a.fp_iters, nullptr, nullptr, 0, 0,
+      uint8_t st = bfgs_solve<float, K, MASK>(G, P, a.iterations, a.fp_iters, nullptr, nullptr, nullptr, 0, 0,
                                               nullptr);
       st |= final_status<float, K, MASK>(G, P);
       conv = (st & FP_STATUS_UNCONVERGED_MASK) == 0;

@@ -34,6 +34,7 @@ struct PathArgs {
   R *T_out, *g_out, *points_out, *length_out;
   uint8_t* status_out;
   R *trace_len, *trace_gnorm, *H_out;
+  uint8_t* trace_fate;  // (iterations, batch) FP_FATE_* bits of each BFGS update (with the trace)
   R *d_basis, *d_anchor, *d_start, *d_end, *u_out;
   // Gathered dispatch (fp_bucket.cu): rows[0 .. n_rows) are this launch's
   // paths (a kind-mask bucket that is not one contiguous range).
@@ -218,8 +219,8 @@ __device__ __forceinline__ void run_path(const PathArgs<R>& a, int64_t row, cons
   uint8_t st = 0;
   P.eval(G, P.g);
   if (OP != OP_VJP)
-    st |= bfgs_solve<R, K, MASK>(G, P, a.iterations, a.fp_iters, a.trace_len, a.trace_gnorm, a.ld, row,
-                                 a.H_out);
+    st |= bfgs_solve<R, K, MASK>(G, P, a.iterations, a.fp_iters, a.trace_len, a.trace_gnorm,
+                                 a.trace_fate, a.ld, row, a.H_out);
   st |= final_status<R, K, MASK>(G, P);
   bool fin = (st & FP_STATUS_NONFINITE) == 0;
 

@@ -458,10 +458,10 @@ struct InvHess {
   // direction p (= -H g_old), curvature flag ok, sy = sg.y and ms =
   // max_j |sg_j|. Out: p = -H' gn with H' the updated matrix (or the old one
   // when the update is skipped: failed curvature test or a non-finite H',
-  // solver.py:184,198).
-  __device__ __forceinline__ void step(const V2<R> (&sg)[NP], const V2<R> (&y)[NP],
-                                       const V2<R> (&gn)[NP], V2<R> (&p)[NP], bool ok, R sy, R ms,
-                                       R nz) {
+  // solver.py:184,198). Returns the update's FP_FATE_* bits.
+  __device__ __forceinline__ uint8_t step(const V2<R> (&sg)[NP], const V2<R> (&y)[NP],
+                                          const V2<R> (&gn)[NP], V2<R> (&p)[NP], bool ok, R sy, R ms,
+                                          R nz) {
     V2<R> Hg[NP];
     mul(gn, Hg, nz);
     if (ok) {
@@ -480,7 +480,9 @@ struct InvHess {
       const R mz = absmaxv<R, NA>(z);
       const R nb = fma(R(2) * ms, mz, bound) * R(1.0009765625);
       bool take = true;
+      uint8_t checked = 0;
       if (!(nb < R(1e36))) {
+        checked = FP_FATE_ENTRY_CHECK;
         // Rare: possible overflow. Check every entry before committing.
         R mx = R(0);
 #pragma unroll
@@ -506,11 +508,15 @@ struct InvHess {
         const R zg = dotv<R, NA>(z, gn, nz), sgn = dotv<R, NA>(sg, gn, nz);
 #pragma unroll
         for (int m = 0; m < NP; ++m) p[m] = fma2(sg[m], bc2(-zg), fma2(z[m], bc2(-sgn), neg2(Hg[m])));
-        return;
+        return checked;
       }
+#pragma unroll
+      for (int m = 0; m < NP; ++m) p[m] = neg2(Hg[m]);
+      return FP_FATE_NONFINITE_SKIP | checked;
     }
 #pragma unroll
     for (int m = 0; m < NP; ++m) p[m] = neg2(Hg[m]);
+    return FP_FATE_CURVATURE_SKIP;
   }
 };
 
@@ -539,7 +545,8 @@ __device__ __forceinline__ void bfgs_iterations(const Geo<R, K>& G, PathState<R,
                                                 InvHess<R, K, MASK>& H,
                                                 V2<R> (&p)[Packed<Lay<K, MASK>::NA>::NP], uint8_t& st,
                                                 int iterations, int fp_iters_rt, R* trace_len,
-                                                R* trace_gnorm, int64_t trace_ld, int64_t row) {
+                                                R* trace_gnorm, uint8_t* trace_fate, int64_t trace_ld,
+                                                int64_t row) {
   using L = Lay<K, MASK>;
   constexpr int NA = L::NA;
   constexpr int NP = Packed<NA>::NP;
@@ -567,13 +574,15 @@ __device__ __forceinline__ void bfgs_iterations(const Geo<R, K>& G, PathState<R,
     const R yy = dotv<R, NA>(y, y, G.nz);
     const bool ok = sy > (R(1e-12) * sqrt_test(ss)) * sqrt_test(yy);
     const R ms = absmaxv<R, NA>(sg);
-    H.step(sg, y, gn, p, ok, sy, ms, G.nz);
+    const uint8_t fate = H.step(sg, y, gn, p, ok, sy, ms, G.nz);
 #pragma unroll
     for (int m = 0; m < NP; ++m) P.g[m] = gn[m];
     if (GENERAL && trace_len != nullptr) {
       P.finish_norms(G);
       trace_len[int64_t(it) * trace_ld + row] = P.length();
       trace_gnorm[int64_t(it) * trace_ld + row] = Num<R>::sqrt_(norm2_seq<R, NA>(P.g));
+      if (trace_fate != nullptr)
+        trace_fate[int64_t(it) * trace_ld + row] = fate | (zero ? FP_FATE_ZERO_DIRECTION : 0);
     }
   }
 }
@@ -585,8 +594,8 @@ __device__ __forceinline__ void bfgs_iterations(const Geo<R, K>& G, PathState<R,
 template <typename R, int K, unsigned MASK>
 __device__ __forceinline__ uint8_t bfgs_solve(const Geo<R, K>& G, PathState<R, K, MASK>& P,
                                               int iterations, int fp_iters, R* trace_len,
-                                              R* trace_gnorm, int64_t trace_ld, int64_t row,
-                                              R* H_out) {
+                                              R* trace_gnorm, uint8_t* trace_fate, int64_t trace_ld,
+                                              int64_t row, R* H_out) {
   using L = Lay<K, MASK>;
   constexpr int NA = L::NA;
   constexpr int NP = Packed<NA>::NP;
@@ -599,11 +608,11 @@ __device__ __forceinline__ uint8_t bfgs_solve(const Geo<R, K>& G, PathState<R, K
   for (int m = 0; m < NP; ++m) p[m] = neg2(P.g[m]);  // H = I
 #ifndef FP_NO_LOOP_SPECIALISATION
   if (fp_iters == 1 && trace_len == nullptr)
-    bfgs_iterations<R, K, MASK, false>(G, P, H, p, st, iterations, 1, nullptr, nullptr, 0, 0);
+    bfgs_iterations<R, K, MASK, false>(G, P, H, p, st, iterations, 1, nullptr, nullptr, nullptr, 0, 0);
   else
 #endif
     bfgs_iterations<R, K, MASK, true>(G, P, H, p, st, iterations, fp_iters, trace_len, trace_gnorm,
-                                      trace_ld, row);
+                                      trace_fate, trace_ld, row);
   P.finish_norms(G);
   if (H_out != nullptr) {
     R* Ho = H_out + row * (4 * K * K);

@@ -465,6 +465,7 @@ __global__ void __launch_bounds__(kWideThreads) wide_kernel(const __grid_constan
       bool zero;
       const R alpha = wide_step_size(c, p, a.fp_iters, zero);
       if (zero) st |= FP_STATUS_ZERO_DIRECTION;
+      uint8_t fate = zero ? FP_FATE_ZERO_DIRECTION : 0;
       for (int j = lane; j < m; j += 32) {
         stp[j] = alpha * p[j];
         t[j] = t[j] + stp[j];
@@ -476,6 +477,7 @@ __global__ void __launch_bounds__(kWideThreads) wide_kernel(const __grid_constan
       const R sy = wide_dot(c, stp, y);
       const R sn = Num<R>::sqrt_(wide_dot(c, stp, stp));
       const R yn = Num<R>::sqrt_(wide_dot(c, y, y));
+      if (!(sy > (R(1e-12) * sn) * yn)) fate |= FP_FATE_CURVATURE_SKIP;
       if (sy > (R(1e-12) * sn) * yn) {
         const R rho = R(1) / sy;
         wide_matvec(c, y, hy, R(1));
@@ -489,6 +491,7 @@ __global__ void __launch_bounds__(kWideThreads) wide_kernel(const __grid_constan
             fin = fin && finite(v);
           }
         }
+        if (!__all_sync(0xffffffffu, fin)) fate |= FP_FATE_NONFINITE_SKIP;
         if (__all_sync(0xffffffffu, fin)) {
           for (int j = lane; j < m; j += 32) {
             R* h = H + j * L.ld;
@@ -506,6 +509,7 @@ __global__ void __launch_bounds__(kWideThreads) wide_kernel(const __grid_constan
         if (lane == 0) {
           a.trace_len[int64_t(it) * a.ld + row] = len;
           a.trace_gnorm[int64_t(it) * a.ld + row] = Num<R>::sqrt_(gq);
+          if (a.trace_fate != nullptr) a.trace_fate[int64_t(it) * a.ld + row] = fate;
         }
       }
     }

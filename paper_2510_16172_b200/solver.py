@@ -68,6 +68,7 @@ class SolveResult:
     trace_len: torch.Tensor | None = None    # (I, B)
     trace_gnorm: torch.Tensor | None = None  # (I, B)
     H: torch.Tensor | None = None            # (B, 2K, 2K)
+    trace_fate: torch.Tensor | None = None   # (I, B) uint8 FATE_* bits of each BFGS update
 
     @property
     def converged(self) -> torch.Tensor:
@@ -111,11 +112,13 @@ def solve(scene: BatchScene, T0=None, opts: SolveOptions = SolveOptions(), *,
         trace_len=_empty((I if K else 0, B), dt, dev) if opts.record_trace else None,
         trace_gnorm=_empty((I if K else 0, B), dt, dev) if opts.record_trace else None,
         H=_empty((B, 2 * K, 2 * K), dt, dev) if return_state else None,
+        trace_fate=_empty((I if K else 0, B), torch.uint8, dev) if opts.record_trace else None,
     )
     fn = lib.fp_solve_f32 if dt == torch.float32 else lib.fp_solve_f64
     rc = fn(ptr(sc.basis), ptr(sc.anchor), ptr(sc.start), ptr(sc.end), ptr(T0), B, K, I,
             opts.fixed_point_iters, ptr(res.T), ptr(res.g), ptr(res.points), ptr(res.length),
-            ptr(res.status), ptr(res.trace_len), ptr(res.trace_gnorm), ptr(res.H), stream_ptr())
+            ptr(res.status), ptr(res.trace_len), ptr(res.trace_gnorm), ptr(res.trace_fate), ptr(res.H),
+            stream_ptr())
     _lib.check(rc, "fp_solve")
     if K == 0:
         res.T.zero_()

@@ -26,9 +26,12 @@ def test_error_strings_and_argument_validation():
     assert b"unsupported" in lib.fp_error_string(2)
     # validation happens before any CUDA call: safe without a GPU
     null = None
-    assert lib.fp_solve_f32(null, null, null, null, null, -1, 2, 10, 1, *([null] * 8), null) == 1
-    assert lib.fp_solve_f32(null, null, null, null, null, 4, 2, 0, 1, *([null] * 8), null) == 1
-    assert lib.fp_solve_f32(null, null, null, null, null, 4, 99, 10, 1, *([null] * 8), null) == 2
+    assert lib.fp_solve_f32(null, null, null, null, null, -1, 2, 10, 1, *([null] * 9), null) == 1
+    assert lib.fp_solve_f32(null, null, null, null, null, 4, 2, 0, 1, *([null] * 9), null) == 1
+    assert lib.fp_solve_f32(null, null, null, null, null, 4, 99, 10, 1, *([null] * 9), null) == 2
+    fate = np.zeros(8, np.uint8)
+    assert lib.fp_solve_f32(null, null, null, null, null, 4, 2, 10, 1, *([null] * 7), fate.ctypes.data,
+                            null, null) == 1  # fates need the trace
     assert lib.fp_vjp_f32(*([null] * 7), 1.0, 7, 4, 2, *([null] * 6), null) == 4
     with pytest.raises(NotImplementedError):
         _lib.check(2, "x")

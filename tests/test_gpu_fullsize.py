@@ -87,3 +87,32 @@ def test_oracle_subsample_full_size(full):
                       (grads.basis, grads.anchor, grads.start, grads.end)))
     err = grad_rel_err(got, flat_grad(db, da, d0, d1))
     assert np.all(err[okg] <= GRAD_REL)
+
+
+@pytest.mark.parametrize("K", [1, 2, 3, 4, 5])
+def test_converged_gate_confusion_full_size(K):
+    """Config 2 at full size (2^22 paths) for every order: on a 2048-path
+    subsample, the device's fp32 convergence gate (the count behind bench
+    `value`) against the oracle's fp64 classification at the reference T
+    (parity.converged_mask), both ways. False positives (device converged,
+    oracle not) and false negatives each stay below 1% of the sample, and
+    every oracle-converged path is in tolerance."""
+    b = datagen.config2(K)
+    sc = BatchScene(b.basis, b.anchor, b.start, b.end)
+    res, _ = solve_with_gradients(sc, b.T0, SolveOptions(iterations=20, precision=Precision.SINGLE))
+    idx = np.sort(np.random.default_rng(100 + K).choice(b.size, 2048, replace=False))
+    it = torch.as_tensor(idx, device=res.T.device)
+    dev = res.converged[it].cpu().numpy()
+    args = (b.basis[idx], b.anchor[idx], b.start[idx], b.end[idx])
+    ref = O.solve_outputs(*args, b.T0[idx], 20, 1, np.float32)
+    conv = converged_mask(*args, ref["T"])
+    fp = float((dev & ~conv).mean())
+    fn = float((~dev & conv).mean())
+    print(f"K={K}: device {dev.mean():.4f} oracle {conv.mean():.4f} FP {fp:.5f} FN {fn:.5f}")
+    assert fp <= 0.01 and fn <= 0.01, (fp, fn)
+    pts = res.points[it].double().cpu().numpy()
+    L = res.length[it].cpu().numpy()
+    ok = points_ok(pts, ref["points"]) & lengths_ok(L, ref["L"])
+    assert ok[conv].all()
+    del res
+    torch.cuda.empty_cache()

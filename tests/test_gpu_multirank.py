@@ -62,7 +62,7 @@ def _worker(rank, world, port, q):
     try:
         res = trace(_scene(), max_order=3, iterations=20, with_grad=True, gather=True)
         recs = [(o.order, o.candidates, o.valid, o.rx.cpu().numpy(), o.seq.cpu().numpy(),
-                 o.T.cpu().numpy(), o.L.cpu().numpy()) for o in res.orders]
+                 o.T.cpu().numpy(), o.length.cpu().numpy()) for o in res.orders]
         grad = (res.loss, res.tx_grad.cpu().numpy(), res.obj_grad.cpu().numpy(),
                 res.vertex_grad.cpu().numpy())
         # config-2 step: rank r takes rows [lo, hi) of the batch
@@ -112,7 +112,7 @@ def test_two_ranks_shard_trace_and_step():
             assert np.array_equal(rx[a], o.rx.cpu().numpy()[b2])
             assert np.array_equal(seq[a], o.seq.cpu().numpy()[b2])
             assert np.array_equal(T[a], o.T.cpu().numpy()[b2])  # per-path results are bitwise
-            assert np.array_equal(L[a], o.L.cpu().numpy()[b2])
+            assert np.array_equal(L[a], o.length.cpu().numpy()[b2])
         rel = lambda x, y: np.linalg.norm(x - y) / max(np.linalg.norm(y), 1e-300)  # noqa: E731
         assert abs(loss - ref.loss) <= 1e-9 * abs(ref.loss)
         assert rel(tx, ref.tx_grad.cpu().numpy()) <= 1e-9

@@ -190,3 +190,29 @@ def test_near_singular_fallback():
         plain = np.linalg.solve(H, -d["v"][j].ravel())
         gap = np.linalg.norm(u.ravel() - plain) / np.linalg.norm(plain)
         assert (gap > 1e-3) == bool(d["fired"][j]), (j, gap)
+
+
+def test_installed_reference_agrees_with_the_port():
+    """bench.py --impl reference times the genuine reference from oracle/_ref
+    (oracle/build_ref.py); on the same sample its forward solve equals the
+    numpy port bit for bit, and the per-path gradient gate accepts the same
+    paths."""
+    import sys
+
+    from oracle.cpu_baseline import REF_DIR, reference_available
+
+    if not reference_available():
+        pytest.skip("oracle/_ref not installed (python oracle/build_ref.py)")
+    sys.path.insert(0, REF_DIR)
+    try:
+        from fermatpath.batching import BatchScene
+        from fermatpath.solver import Precision, SolveOptions, _bfgs_kernel
+    finally:
+        sys.path.remove(REF_DIR)
+    from paper_2510_16172_b200 import datagen
+
+    b = datagen.config2(3, 256)
+    T, g, _ = _bfgs_kernel(BatchScene(b.basis, b.anchor, b.start, b.end), b.T0,
+                           SolveOptions(iterations=20, precision=Precision.SINGLE))
+    r = O.bfgs(b.basis, b.anchor, b.start, b.end, b.T0, 20, 1, np.float32)
+    assert np.array_equal(T, r["T"]) and np.array_equal(g, r["g"])
