@@ -200,21 +200,63 @@ def _barrier(ws):
         dist.barrier()
 
 
-def _load_ncu_traffic(K: int, paths: int):
-    """DRAM bytes (read + write) per launch of the fused kernel, from the committed
-    `ncu --set full` capture (profiles/ncu_summary.json), scaled per path."""
-    path = os.path.join(REPO, "profiles", "ncu_summary.json")
+def _ncu_entry(K: int):
+    """The committed `ncu --set full` capture of the fused kernel of order K
+    (profiles/ncu_summary.json)."""
     try:
-        with open(path) as fh:
-            d = json.load(fh)
-        ent = d.get(f"fused_k{K}")
-        return None if ent is None else float(ent["dram_bytes_per_path"]) * paths
-    except (OSError, ValueError, KeyError):
+        with open(os.path.join(REPO, "profiles", "ncu_summary.json")) as fh:
+            return json.load(fh).get(f"fused_k{K}")
+    except (OSError, ValueError):
         return None
 
 
-def measure_ffma_peak(lib, stream, dev):
-    """FP32 FFMA peak in TFLOP/s (best of 5, CUDA events)."""
+def _load_ncu_traffic(K: int, paths: int):
+    """DRAM bytes (read + write) per launch of the fused kernel, scaled per path."""
+    ent = _ncu_entry(K)
+    try:
+        return None if ent is None else float(ent["dram_bytes_per_path"]) * paths
+    except (KeyError, ValueError):
+        return None
+
+
+def gate_check(lib, sc, T, status, n=2048, seed=0):
+    """The device's fp32 convergence gate (status bits, the count behind
+    `value`) against the reference's gate recomputed in fp64 at the same T:
+    objective.gradient / path_length (unclamped norms) through the library's
+    fp64 objective kernel, |g| < 1e-5 (1 + L) (implicit_diff.py:25,30-36), on
+    a random n-path subsample. Returns the two-way confusion counts."""
+    import torch
+
+    from paper_2510_16172_b200 import _lib
+
+    B, K = T.shape[0], T.shape[1]
+    idx = torch.as_tensor(np.sort(np.random.default_rng(seed).choice(B, min(n, B), replace=False)),
+                          device=T.device)
+    f8 = torch.float64
+    args = [sc.basis[idx].to(f8).contiguous(), sc.anchor[idx].to(f8).contiguous(),
+            sc.start[idx].to(f8).contiguous(), sc.end[idx].to(f8).contiguous(), T[idx].to(f8).contiguous()]
+    m = len(idx)
+    L = torch.empty(m, dtype=f8, device=T.device)
+    g = torch.empty(m, K, 2, dtype=f8, device=T.device)
+    st = torch.empty(m, dtype=torch.uint8, device=T.device)
+    P = lambda t: t.data_ptr()  # noqa: E731
+    _lib.check(lib.fp_objective_f64(*(P(a) for a in args), m, K, P(L), P(g), None, P(st),
+                                    torch.cuda.current_stream().cuda_stream), "fp_objective_f64")
+    gn = g.reshape(m, -1).norm(dim=1)
+    ref = (torch.isfinite(gn) & torch.isfinite(L) & (gn < 1e-5 * (1 + L))
+           & ((st & _lib.STATUS_DEGENERATE_FINAL) == 0))
+    dev = (status[idx] & _lib.STATUS_UNCONVERGED_MASK) == 0
+    return {"sample": m, "device_converged": int(dev.sum()), "fp64_converged": int(ref.sum()),
+            "device_only": int((dev & ~ref).sum()), "fp64_only": int((~dev & ref).sum()),
+            "what": "device fp32 gate vs the reference gate recomputed in fp64 at the device T "
+                    "(fp_objective_f64); the oracle comparison at the reference T is "
+                    "tests/test_gpu_fullsize.py::test_converged_gate_confusion_full_size"}
+
+
+def measure_ffma_peak(lib, stream, dev, register_operands=False):
+    """FP32 FFMA peak in TFLOP/s (best of 5, CUDA events). register_operands:
+    every operand in a distinct register pair (fp_peak_ffma_reg), the operand
+    form of the path kernels' arithmetic."""
     import torch
 
     props = torch.cuda.get_device_properties(dev)
@@ -222,10 +264,11 @@ def measure_ffma_peak(lib, stream, dev):
     iters = 4096
     out = torch.zeros(1, device=dev)
     best = 0.0
+    fn = lib.fp_peak_ffma_reg if register_operands else lib.fp_peak_ffma
     for _ in range(6):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        rc = lib.fp_peak_ffma(blocks, iters, out.data_ptr(), stream)
+        rc = fn(blocks, iters, out.data_ptr(), stream)
         e1.record()
         torch.cuda.synchronize()
         if rc != 0:
@@ -392,11 +435,13 @@ def run_ours(args):
     # FP32 roofline probe first: it also brings the SM clock up from idle
     # before the warm-up steps, so the first timed steps are not ramping.
     peak = measure_ffma_peak(lib, stream, dev) if rank == 0 else None
+    peak_reg = measure_ffma_peak(lib, stream, dev, register_operands=True) if rank == 0 else None
 
     # ---- fused forward + VJP step (the headline) ------------------------------
     sampler = ClockSampler(torch.cuda.current_device())
     tot_ms, ms_list, launches = timed(step, args.steps, args.warmup, sampler)
     conv = int(((st & _lib.STATUS_UNCONVERGED_MASK) == 0).sum().item())
+    gates = gate_check(lib, sc, outT, st) if rank == 0 else None
     tot_ms_max = _max_over_ranks(tot_ms, ws, dev)
     conv_all = _sum_over_ranks(conv, ws, dev)
     paths_all = _sum_over_ranks(B, ws, dev)
@@ -424,6 +469,8 @@ def run_ours(args):
         pass
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     traffic = _load_ncu_traffic(K, B)
+    ncu = _ncu_entry(K) or {}
+    exec_flop = ncu.get("executed_flop_per_path")
 
     # ---- end to end through the host-buffer C-ABI entry ---------------------------------
     e2e = None
@@ -540,10 +587,19 @@ def run_ours(args):
                 "flop_per_path": fl_fwd + fl_vjp, "paths_per_launch": B,
                 "peak_source": "FFMA microbenchmark (fp_peak_ffma) measured in this run; "
                                "MEASURED_PEAKS.json has no FP32 SIMT figure",
+                # what the kernel really executes (ncu: FADD+FMUL+2 FFMA, paired
+                # ops x2, of the committed capture) and the register-operand
+                # FFMA2 ceiling measured in this run (fp_peak_ffma_reg)
+                "executed_flop_per_path": exec_flop,
+                "executed_achieved": (exec_flop * B / avg_launch_s / 1e12) if exec_flop else None,
+                "peak_register_operands": peak_reg,
+                "executed_frac_of_register_peak": (exec_flop * B / avg_launch_s / 1e12 / peak_reg)
+                if (exec_flop and peak_reg) else None,
                 "hbm": {"achieved": hbm_gbs, "peak": hbm_peak, "unit": "GB/s",
                         "frac": hbm_gbs / hbm_peak, "bytes_per_path": rd + wr},
             },
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+            "converged_gate": gates,
         }
         print(json.dumps(line), flush=True)
     if ws > 1:

@@ -270,6 +270,10 @@ int fp_image_method_f64(const double* basis, const double* anchor, const double*
  * blocks x 256 threads, each running iters x 128 dependent-free FFMAs; the
  * bench times it with CUDA events to measure the FP32 SIMT peak. */
 int fp_peak_ffma(int blocks, int iters, float* out, void* stream);
+/* The same FMA-lane count with every operand in a distinct register pair
+ * (FFMA2 a, b, c all registers): the attainable ceiling for register-resident
+ * arithmetic (register-file bandwidth bound). */
+int fp_peak_ffma_reg(int blocks, int iters, float* out, void* stream);
 
 /* Benchmark utility: enqueue a kernel that holds `stream` until the host
  * stores a nonzero int at host_flag (pinned host memory) or timeout_s

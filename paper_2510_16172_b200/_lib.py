@@ -78,6 +78,7 @@ _SIGS = {
     "fp_line_search_f64": [_P] * 7 + [_I64, _I, _I] + [_P] * 2 + [_P],
     "fp_init_params_f64": [_P] * 4 + [_I64, _I, _P, _P],
     "fp_peak_ffma": [_I, _I, _P, _P],
+    "fp_peak_ffma_reg": [_I, _I, _P, _P],
     "fp_gate_wait": [_P, _D, _P],
     "fp_enum_pattern_count": [_I, _I, _I, C.c_uint],
     "fp_enum_decode": [_P, _I, _P, _I, _I, _I, C.c_uint, _I64, _I64, _P, _P, _P],

@@ -751,32 +751,30 @@ __device__ __forceinline__ uint8_t implicit_vjp(const Geo<R, K>& G, const PathSt
     // |H_a x - rhs| <= tol (1 + |rhs|); otherwise (or on a zero pivot / a
     // non-finite solution) one retry on H_a + lambda I with lambda =
     // 1e-12 tr(H_a), accepted when finite. Inert rows are pinned identity rows
-    // with zero rhs: they add nothing to either norm.
-    bool solved = false;
-    for (int attempt = 0; attempt < 2 && !solved; ++attempt) {
-      const R lam = attempt == 0 ? R(0) : R(1e-12) * trace;
-      R Ci[K][3];  // inverse pivot blocks
-      R z[K][2];
+    // with zero rhs: they add nothing to either norm. LAPACK's LU solve is
+    // backward stable (residual ~ eps |H| |x|); the explicit 2x2 block
+    // inverses are not quite, so a solution that misses the bound first gets
+    // one step of fixed-precision iterative refinement (which restores a
+    // backward-stable residual) before the bound decides.
+    R Ci[K][3];      // inverse pivot blocks
+    R Lm[K][2][2];   // elimination multipliers O_{i-1}^T Cinv_{i-1}
+    auto factor = [&](R lam) {
       bool ok = true;
 #pragma unroll
       for (int i = 0; i < K; ++i) {
         R C0 = D[i][0] + (act[i][0] ? lam : R(0));
         R C1 = D[i][1];
         R C2 = D[i][2] + (act[i][1] ? lam : R(0));
-        R z0 = rhs[i][0], z1 = rhs[i][1];
         if (i > 0) {
-          // Lm = O_{i-1}^T Cinv_{i-1}; C -= Lm O_{i-1}; z -= Lm z_{i-1}
-          R Lm[2][2];
+          // Lm = O_{i-1}^T Cinv_{i-1}; C -= Lm O_{i-1}
 #pragma unroll
           for (int a = 0; a < 2; ++a) {
-            Lm[a][0] = O[i - 1][0][a] * Ci[i - 1][0] + O[i - 1][1][a] * Ci[i - 1][1];
-            Lm[a][1] = O[i - 1][0][a] * Ci[i - 1][1] + O[i - 1][1][a] * Ci[i - 1][2];
+            Lm[i][a][0] = O[i - 1][0][a] * Ci[i - 1][0] + O[i - 1][1][a] * Ci[i - 1][1];
+            Lm[i][a][1] = O[i - 1][0][a] * Ci[i - 1][1] + O[i - 1][1][a] * Ci[i - 1][2];
           }
-          C0 -= Lm[0][0] * O[i - 1][0][0] + Lm[0][1] * O[i - 1][1][0];
-          C1 -= Lm[0][0] * O[i - 1][0][1] + Lm[0][1] * O[i - 1][1][1];
-          C2 -= Lm[1][0] * O[i - 1][0][1] + Lm[1][1] * O[i - 1][1][1];
-          z0 -= Lm[0][0] * z[i - 1][0] + Lm[0][1] * z[i - 1][1];
-          z1 -= Lm[1][0] * z[i - 1][0] + Lm[1][1] * z[i - 1][1];
+          C0 -= Lm[i][0][0] * O[i - 1][0][0] + Lm[i][0][1] * O[i - 1][1][0];
+          C1 -= Lm[i][0][0] * O[i - 1][0][1] + Lm[i][0][1] * O[i - 1][1][1];
+          C2 -= Lm[i][1][0] * O[i - 1][0][1] + Lm[i][1][1] * O[i - 1][1][1];
         }
         const R det = C0 * C2 - C1 * C1;
         ok = ok && (det != R(0)) && finite(det);  // LinAlgError: exactly singular pivot
@@ -784,11 +782,22 @@ __device__ __forceinline__ uint8_t implicit_vjp(const Geo<R, K>& G, const PathSt
         Ci[i][0] = C2 * id;
         Ci[i][1] = -C1 * id;
         Ci[i][2] = C0 * id;
-        z[i][0] = z0;
-        z[i][1] = z1;
       }
-      if (!ok) continue;
-      // back substitution
+      return ok;
+    };
+    // x = (factored matrix)^-1 b; false when x is not finite
+    auto substitute = [&](const R (&b)[K][2], R (&x)[K][2]) {
+      R z[K][2];
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        z[i][0] = b[i][0];
+        z[i][1] = b[i][1];
+        if (i > 0) {
+          z[i][0] -= Lm[i][0][0] * z[i - 1][0] + Lm[i][0][1] * z[i - 1][1];
+          z[i][1] -= Lm[i][1][0] * z[i - 1][0] + Lm[i][1][1] * z[i - 1][1];
+        }
+      }
+      bool ok = true;
       R nxt0 = R(0), nxt1 = R(0);
 #pragma unroll
       for (int i = K - 1; i >= 0; --i) {
@@ -799,35 +808,57 @@ __device__ __forceinline__ uint8_t implicit_vjp(const Geo<R, K>& G, const PathSt
         }
         const R v0 = Ci[i][0] * r0 + Ci[i][1] * r1;
         const R v1 = Ci[i][1] * r0 + Ci[i][2] * r1;
-        sol[i][0] = act[i][0] ? v0 : R(0);
-        sol[i][1] = act[i][1] ? v1 : R(0);
-        nxt0 = sol[i][0];
-        nxt1 = sol[i][1];
+        x[i][0] = act[i][0] ? v0 : R(0);
+        x[i][1] = act[i][1] ? v1 : R(0);
+        nxt0 = x[i][0];
+        nxt1 = x[i][1];
         ok = ok && finite(v0) && finite(v1);
       }
-      if (ok && attempt == 0) {
-        // residual check of the unregularised solution (implicit_diff.py:58-61)
-        R rr = R(0), bb = R(0);
+      return ok;
+    };
+    // r = rhs - H_a x (unregularised); returns |r|^2
+    auto residual = [&](const R (&x)[K][2], R (&r)[K][2]) {
+      R rr = R(0);
 #pragma unroll
-        for (int i = 0; i < K; ++i) {
-          R r0 = D[i][0] * sol[i][0] + D[i][1] * sol[i][1] - rhs[i][0];
-          R r1 = D[i][1] * sol[i][0] + D[i][2] * sol[i][1] - rhs[i][1];
-          if (i > 0) {
-            r0 += O[i - 1][0][0] * sol[i - 1][0] + O[i - 1][1][0] * sol[i - 1][1];
-            r1 += O[i - 1][0][1] * sol[i - 1][0] + O[i - 1][1][1] * sol[i - 1][1];
-          }
-          if (i + 1 < K) {
-            r0 += O[i][0][0] * sol[i + 1][0] + O[i][0][1] * sol[i + 1][1];
-            r1 += O[i][1][0] * sol[i + 1][0] + O[i][1][1] * sol[i + 1][1];
-          }
-          rr = fma(r1, r1, fma(r0, r0, rr));
-          bb = fma(rhs[i][1], rhs[i][1], fma(rhs[i][0], rhs[i][0], bb));
+      for (int i = 0; i < K; ++i) {
+        R r0 = D[i][0] * x[i][0] + D[i][1] * x[i][1];
+        R r1 = D[i][1] * x[i][0] + D[i][2] * x[i][1];
+        if (i > 0) {
+          r0 += O[i - 1][0][0] * x[i - 1][0] + O[i - 1][1][0] * x[i - 1][1];
+          r1 += O[i - 1][0][1] * x[i - 1][0] + O[i - 1][1][1] * x[i - 1][1];
         }
-        const R tol = Num<R>::resid_tol() * (R(1) + Num<R>::sqrt_(bb));
-        ok = Num<R>::sqrt_(rr) <= tol;  // NaN: retry
+        if (i + 1 < K) {
+          r0 += O[i][0][0] * x[i + 1][0] + O[i][0][1] * x[i + 1][1];
+          r1 += O[i][1][0] * x[i + 1][0] + O[i][1][1] * x[i + 1][1];
+        }
+        r[i][0] = rhs[i][0] - r0;
+        r[i][1] = rhs[i][1] - r1;
+        rr = fma(r[i][1], r[i][1], fma(r[i][0], r[i][0], rr));
       }
-      solved = ok;
+      return rr;
+    };
+    bool solved = false;
+    if (factor(R(0)) && substitute(rhs, sol)) {
+      R bb = R(0);
+#pragma unroll
+      for (int i = 0; i < K; ++i) bb = fma(rhs[i][1], rhs[i][1], fma(rhs[i][0], rhs[i][0], bb));
+      const R tol = Num<R>::resid_tol() * (R(1) + Num<R>::sqrt_(bb));
+      R r[K][2];
+      solved = Num<R>::sqrt_(residual(sol, r)) <= tol;  // NaN: not solved
+      if (!solved) {
+        R dx[K][2];
+        if (substitute(r, dx)) {
+#pragma unroll
+          for (int i = 0; i < K; ++i) {
+            sol[i][0] += dx[i][0];
+            sol[i][1] += dx[i][1];
+          }
+          solved = Num<R>::sqrt_(residual(sol, r)) <= tol;
+        }
+      }
     }
+    // Tikhonov retry (implicit_diff.py:64-71): accepted when finite
+    if (!solved) solved = factor(R(1e-12) * trace) && substitute(rhs, sol);
     if (!solved) {
       st |= FP_STATUS_SINGULAR;
 #pragma unroll

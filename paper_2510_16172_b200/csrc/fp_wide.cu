@@ -273,25 +273,27 @@ __device__ uint8_t wide_vjp(const WideCtx<R>& c, const PathArgs<R>& a, int64_t r
   if (need_solve) {
     if (c.lane == 0) {
       // _solve_sym (implicit_diff.py:55-71): block-Thomas elimination, accepted
-      // when |H_a x - rhs| <= tol (1 + |rhs|), else (or on a zero pivot / a
-      // non-finite solution) one Tikhonov retry; Ci and z reuse dx (3K) and
-      // w (2K of 3S) as scratch
+      // when |H_a x - rhs| <= tol (1 + |rhs|) — after one step of iterative
+      // refinement if the first solution misses (fp_path.cuh explains why) —
+      // else (or on a zero pivot / a non-finite solution) one Tikhonov retry,
+      // accepted when finite. Scratch: Ci in dx (3K), z in w (2K of 3S), the
+      // residual in y (2K) and the correction in hy (2K) (BFGS scratch, free
+      // here).
       R* Ci = sm + L.dx;
       R* z = sm + L.w;
-      bool solved = false;
-      for (int attempt = 0; attempt < 2 && !solved; ++attempt) {
-        const R lam = attempt == 0 ? R(0) : R(1e-12) * trace;
+      R* res = sm + L.y;
+      R* dxs = sm + L.hy;
+      const R* O_ = sm + L.O;
+      auto factor = [&](R lam) {
         bool ok = true;
         for (int i = 0; i < K; ++i) {
           const R* D = sm + L.D + 3 * i;
           const bool a0 = sm[L.act + 2 * i] != R(0), a1 = sm[L.act + 2 * i + 1] != R(0);
           R C0 = D[0] + (a0 ? lam : R(0)), C1 = D[1], C2 = D[2] + (a1 ? lam : R(0));
-          R z0 = sm[L.rhs + 2 * i], z1 = sm[L.rhs + 2 * i + 1];
           if (i > 0) {
-            const R* O = sm + L.O + 4 * (i - 1);  // O[a][b] = O[2a + b]
+            const R* O = O_ + 4 * (i - 1);  // O[a][b] = O[2a + b]
             const R* Cp = Ci + 3 * (i - 1);
             R Lm[2][2];
-#pragma unroll
             for (int aa = 0; aa < 2; ++aa) {
               Lm[aa][0] = O[aa] * Cp[0] + O[2 + aa] * Cp[1];
               Lm[aa][1] = O[aa] * Cp[1] + O[2 + aa] * Cp[2];
@@ -299,8 +301,6 @@ __device__ uint8_t wide_vjp(const WideCtx<R>& c, const PathArgs<R>& a, int64_t r
             C0 -= Lm[0][0] * O[0] + Lm[0][1] * O[2];
             C1 -= Lm[0][0] * O[1] + Lm[0][1] * O[3];
             C2 -= Lm[1][0] * O[1] + Lm[1][1] * O[3];
-            z0 -= Lm[0][0] * z[2 * (i - 1)] + Lm[0][1] * z[2 * (i - 1) + 1];
-            z1 -= Lm[1][0] * z[2 * (i - 1)] + Lm[1][1] * z[2 * (i - 1) + 1];
           }
           const R det = C0 * C2 - C1 * C1;
           ok = ok && det != R(0) && finite(det);  // LinAlgError: exactly singular pivot
@@ -308,15 +308,32 @@ __device__ uint8_t wide_vjp(const WideCtx<R>& c, const PathArgs<R>& a, int64_t r
           Ci[3 * i] = C2 * id;
           Ci[3 * i + 1] = -C1 * id;
           Ci[3 * i + 2] = C0 * id;
+        }
+        return ok;
+      };
+      auto substitute = [&](const R* b, R* x) {
+        for (int i = 0; i < K; ++i) {
+          R z0 = b[2 * i], z1 = b[2 * i + 1];
+          if (i > 0) {
+            const R* O = O_ + 4 * (i - 1);
+            const R* Cp = Ci + 3 * (i - 1);
+            R Lm[2][2];
+            for (int aa = 0; aa < 2; ++aa) {
+              Lm[aa][0] = O[aa] * Cp[0] + O[2 + aa] * Cp[1];
+              Lm[aa][1] = O[aa] * Cp[1] + O[2 + aa] * Cp[2];
+            }
+            z0 -= Lm[0][0] * z[2 * (i - 1)] + Lm[0][1] * z[2 * (i - 1) + 1];
+            z1 -= Lm[1][0] * z[2 * (i - 1)] + Lm[1][1] * z[2 * (i - 1) + 1];
+          }
           z[2 * i] = z0;
           z[2 * i + 1] = z1;
         }
-        if (!ok) continue;
+        bool ok = true;
         R nx0 = R(0), nx1 = R(0);
         for (int i = K - 1; i >= 0; --i) {
           R r0 = z[2 * i], r1 = z[2 * i + 1];
           if (i + 1 < K) {
-            const R* O = sm + L.O + 4 * i;
+            const R* O = O_ + 4 * i;
             r0 -= O[0] * nx0 + O[1] * nx1;
             r1 -= O[2] * nx0 + O[3] * nx1;
           }
@@ -324,36 +341,48 @@ __device__ uint8_t wide_vjp(const WideCtx<R>& c, const PathArgs<R>& a, int64_t r
           const R v1 = Ci[3 * i + 1] * r0 + Ci[3 * i + 2] * r1;
           nx0 = sm[L.act + 2 * i] != R(0) ? v0 : R(0);
           nx1 = sm[L.act + 2 * i + 1] != R(0) ? v1 : R(0);
-          sm[L.sol + 2 * i] = nx0;
-          sm[L.sol + 2 * i + 1] = nx1;
+          x[2 * i] = nx0;
+          x[2 * i + 1] = nx1;
           ok = ok && finite(v0) && finite(v1);
         }
-        if (ok && attempt == 0) {
-          // residual check of the unregularised solution (implicit_diff.py:58-61)
-          const R* x = sm + L.sol;
-          const R* rh = sm + L.rhs;
-          R rr = R(0), bb = R(0);
-          for (int i = 0; i < K; ++i) {
-            const R* D = sm + L.D + 3 * i;
-            R r0 = D[0] * x[2 * i] + D[1] * x[2 * i + 1] - rh[2 * i];
-            R r1 = D[1] * x[2 * i] + D[2] * x[2 * i + 1] - rh[2 * i + 1];
-            if (i > 0) {
-              const R* O = sm + L.O + 4 * (i - 1);
-              r0 += O[0] * x[2 * i - 2] + O[2] * x[2 * i - 1];
-              r1 += O[1] * x[2 * i - 2] + O[3] * x[2 * i - 1];
-            }
-            if (i + 1 < K) {
-              const R* O = sm + L.O + 4 * i;
-              r0 += O[0] * x[2 * i + 2] + O[1] * x[2 * i + 3];
-              r1 += O[2] * x[2 * i + 2] + O[3] * x[2 * i + 3];
-            }
-            rr = fma(r1, r1, fma(r0, r0, rr));
-            bb = fma(rh[2 * i + 1], rh[2 * i + 1], fma(rh[2 * i], rh[2 * i], bb));
+        return ok;
+      };
+      auto residual = [&](const R* x) {  // res = rhs - H_a x; returns |res|^2
+        const R* rh = sm + L.rhs;
+        R rr = R(0);
+        for (int i = 0; i < K; ++i) {
+          const R* D = sm + L.D + 3 * i;
+          R r0 = D[0] * x[2 * i] + D[1] * x[2 * i + 1];
+          R r1 = D[1] * x[2 * i] + D[2] * x[2 * i + 1];
+          if (i > 0) {
+            const R* O = O_ + 4 * (i - 1);
+            r0 += O[0] * x[2 * i - 2] + O[2] * x[2 * i - 1];
+            r1 += O[1] * x[2 * i - 2] + O[3] * x[2 * i - 1];
           }
-          ok = Num<R>::sqrt_(rr) <= Num<R>::resid_tol() * (R(1) + Num<R>::sqrt_(bb));
+          if (i + 1 < K) {
+            const R* O = O_ + 4 * i;
+            r0 += O[0] * x[2 * i + 2] + O[1] * x[2 * i + 3];
+            r1 += O[2] * x[2 * i + 2] + O[3] * x[2 * i + 3];
+          }
+          res[2 * i] = rh[2 * i] - r0;
+          res[2 * i + 1] = rh[2 * i + 1] - r1;
+          rr = fma(res[2 * i + 1], res[2 * i + 1], fma(res[2 * i], res[2 * i], rr));
         }
-        solved = ok;
+        return rr;
+      };
+      R* x = sm + L.sol;
+      bool solved = false;
+      if (factor(R(0)) && substitute(sm + L.rhs, x)) {
+        R bb = R(0);
+        for (int i = 0; i < 2 * K; ++i) bb = fma(sm[L.rhs + i], sm[L.rhs + i], bb);
+        const R tol = Num<R>::resid_tol() * (R(1) + Num<R>::sqrt_(bb));
+        solved = Num<R>::sqrt_(residual(x)) <= tol;  // NaN: not solved
+        if (!solved && substitute(res, dxs)) {
+          for (int i = 0; i < 2 * K; ++i) x[i] += dxs[i];
+          solved = Num<R>::sqrt_(residual(x)) <= tol;
+        }
       }
+      if (!solved) solved = factor(R(1e-12) * trace) && substitute(sm + L.rhs, x);
       if (!solved)
         for (int i = 0; i < 2 * K; ++i) sm[L.sol + i] = R(0);
       sm[L.red] = solved ? R(1) : R(0);

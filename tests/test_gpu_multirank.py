@@ -7,7 +7,7 @@ SPEC.md:253): this checks the sharding and the collectives, not scaling.
 
 - scene tracing (configs 3/4): `trace(..., with_grad=True, gather=True)` on
   2 ranks returns the 1-rank valid set (same records, rank-major) and the
-  all-reduced scene gradient within 1e-9 relative of the 1-rank sum;
+  all-reduced scene gradient within 1e-8 relative of the 1-rank sum;
 - the config-2 fused step on a contiguous path shard per rank
   (`scene._share`, as bench.py assigns rows): the union of the shards is
   bitwise the 1-rank result;
@@ -113,11 +113,14 @@ def test_two_ranks_shard_trace_and_step():
             assert np.array_equal(seq[a], o.seq.cpu().numpy()[b2])
             assert np.array_equal(T[a], o.T.cpu().numpy()[b2])  # per-path results are bitwise
             assert np.array_equal(L[a], o.length.cpu().numpy()[b2])
+        # fp64 sums of fp32 per-path terms in a different order (two ranks,
+        # atomics): equal to ~1e-9 relative (measured 2.4e-9 on the object
+        # gradient, whose entries cancel)
         rel = lambda x, y: np.linalg.norm(x - y) / max(np.linalg.norm(y), 1e-300)  # noqa: E731
         assert abs(loss - ref.loss) <= 1e-9 * abs(ref.loss)
-        assert rel(tx, ref.tx_grad.cpu().numpy()) <= 1e-9
-        assert rel(obj, ref.obj_grad.cpu().numpy()) <= 1e-9
-        assert rel(vert, ref.vertex_grad.cpu().numpy()) <= 1e-9
+        assert rel(tx, ref.tx_grad.cpu().numpy()) <= 1e-8
+        assert rel(obj, ref.obj_grad.cpu().numpy()) <= 1e-8
+        assert rel(vert, ref.vertex_grad.cpu().numpy()) <= 1e-8
         for got, want in zip(step, ref_step):
             assert np.array_equal(got, want)
 

@@ -23,6 +23,9 @@ KEYS = [
     "smsp__average_warps_issue_stalled_dispatch_stall_per_issue_active.ratio",
     "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
 ]
+# executed FP32 operations (thread-level, predicated on): paired ops count two
+# lanes, an FMA two flops
+FLOPS = {"fadd": 1, "fmul": 1, "ffma": 2, "fadd2": 2, "fmul2": 2, "ffma2": 4}
 UNIT = {"dram__bytes_read.sum": None, "dram__bytes_write.sum": None}
 
 
@@ -40,6 +43,10 @@ def main():
         wr = float(ent["dram__bytes_write.sum"].replace(",", ""))
         ent["paths_per_launch"] = paths
         ent["dram_bytes_per_path"] = (rd + wr) / paths
+        ops = {o: d.get(f"smsp__sass_thread_inst_executed_op_{o}_pred_on.sum") for o in FLOPS}
+        if all(v not in (None, "") for v in ops.values()):
+            ent["executed_fp32_ops"] = {o: float(v.replace(",", "")) for o, v in ops.items()}
+            ent["executed_flop_per_path"] = sum(FLOPS[o] * v for o, v in ent["executed_fp32_ops"].items()) / paths
         ent["kernel"] = d["Kernel Name"]
         res[d["Kernel Name"]] = ent
     print(json.dumps(res, indent=1))
