@@ -186,3 +186,31 @@ def bfgs_parallel(basis, anchor, start, end, T0, iters, dtype=np.float32, chunk=
         else:
             os.environ["OMP_NUM_THREADS"] = env_threads
     return np.concatenate(out)
+
+
+def _full_grad_rows(args):
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from oracle import fermat_oracle as O
+
+    basis, anchor, start, end, T, weights = args
+    return O.full_gradient_rows(basis, anchor, start, end, T, np.arange(len(T)), weights)
+
+
+def full_gradient_parallel(basis, anchor, start, end, T, weights=None, chunk=4096,
+                           cores: int | None = None):
+    """oracle.full_gradient_rows over every row, in chunks on the host cores."""
+    n = len(T)
+    jobs = [(basis[lo:lo + chunk], anchor[lo:lo + chunk], start[lo:lo + chunk], end[lo:lo + chunk],
+             T[lo:lo + chunk], None if weights is None else weights[lo:lo + chunk])
+            for lo in range(0, n, chunk)]
+    env_threads = os.environ.get("OMP_NUM_THREADS")
+    os.environ["OMP_NUM_THREADS"] = "1"
+    try:
+        with mp.get_context("spawn").Pool(max(1, min(cores or host_cores(), len(jobs)))) as pool:
+            out = pool.map(_full_grad_rows, jobs)
+    finally:
+        if env_threads is None:
+            os.environ.pop("OMP_NUM_THREADS", None)
+        else:
+            os.environ["OMP_NUM_THREADS"] = env_threads
+    return tuple(np.concatenate([o[i] for o in out]) for i in range(5))

@@ -215,11 +215,12 @@ struct PathState {
     for (int k = 1; k < S; ++k) l += nu[k];
     return l;
   }
-  // Shortest segment (NaN-blind like the reference's `norms <= eps` test).
+  // Shortest segment over the non-NaN norms (NaN only if all are): `m <= eps`
+  // is the reference's np.any(norms <= eps) (batching.py:107-114).
   __device__ __forceinline__ R min_norm() const {
     R m = nu[0];
 #pragma unroll
-    for (int k = 1; k < S; ++k) m = nu[k] < m ? nu[k] : m;
+    for (int k = 1; k < S; ++k) m = (nu[k] < m || m != m) ? nu[k] : m;
     return m;
   }
 
@@ -279,11 +280,12 @@ struct PathState {
     }
     if (LIGHT) {
       // reciprocal clamped norms of two segments per paired refinement
+      const R eps2 = G.eps * G.eps;
 #pragma unroll
-      for (int m = 0; m < S / 2; ++m) rcp_norm2(qp[m], G.eps, G.reps, rnp[m]);
+      for (int m = 0; m < S / 2; ++m) rcp_norm2(qp[m], G.eps, eps2, G.reps, rnp[m]);
       if constexpr (S & 1) {
         R r;
-        rcp_norm(qp[SP - 1].x, G.eps, G.reps, r);
+        rcp_norm(qp[SP - 1].x, G.eps, eps2, G.reps, r);
         rnp[SP - 1] = mk2(r, R(0));
       }
     } else {
@@ -470,27 +472,46 @@ struct InvHess {
       for (int m = 0; m < NP; ++m) Hy[m] = add2(Hg[m], p[m]);
       const R rho = rcp_fast(sy);
       const R yHy = dotv<R, NA>(y, Hy, nz);
-      const R half = R(0.5) * fma(rho * rho, yHy, rho);
+      const R rr = rho * rho;
+      const R half = R(0.5) * fma(rr, yHy, rho);
       V2<R> z[NP];
 #pragma unroll
       for (int m = 0; m < NP; ++m) z[m] = fma2(bc2(half), sg[m], mul2(bc2(-rho), Hy[m]));
       // |H'_ij| <= bound + |z_i s_j + s_i z_j| <= bound + 2 max|s| max|z|.
-      // The magnitudes are FMNMX (ALU pipe) reductions; NaN/inf propagate
-      // into nb and send the update through the per-entry check.
+      // The reference evaluates H' as H - rho (s Hy^T + Hy s^T) + (rho^2 yHy +
+      // rho) s s^T, whose intermediates (s_i s_j, s_i Hy_j, rho^2, rho^2 yHy,
+      // the rank-one coefficient times s_i s_j) can overflow in fp32 where
+      // the two-term form does not — and then it skips the update
+      // (solver.py:196-199). So the update is "suspect" when any of those
+      // magnitudes, or the bound on H', reaches 1e36 (far above every healthy
+      // path, 340x below FLT_MAX); suspect updates evaluate the reference's
+      // expression entry by entry. The magnitudes are FMNMX (ALU pipe)
+      // reductions; NaN/inf propagate into `sus` and send the update down
+      // the checked path too.
       const R mz = absmaxv<R, NA>(z);
       const R nb = fma(R(2) * ms, mz, bound) * R(1.0009765625);
+      const R mhy = absmaxv<R, NA>(Hy);
+      const R smax = ms * absmax_nan(ms, mhy);  // >= |s_i s_j|, |s_i Hy_j|
+      R sus = absmax_nan(nb, smax * (R(4) * rho));
+      sus = absmax_nan(sus, rr * absmax_nan(yHy, R(1)));
+      sus = absmax_nan(sus, smax * (R(4) * half));
       bool take = true;
       uint8_t checked = 0;
-      if (!(nb < R(1e36))) {
+      if (!(sus < R(1e36))) {
         checked = FP_FATE_ENTRY_CHECK;
-        // Rare: possible overflow. Check every entry before committing.
+        // Rare: possible overflow. Check every entry before committing, in
+        // the reference's evaluation order and in the committed form.
+        const R coef = rr * yHy + rho;  // (rho rho) yHy + rho, unfused like numpy
         R mx = R(0);
 #pragma unroll
         for (int r = 0; r < NA; ++r)
 #pragma unroll
           for (int c = r; c < NA; ++c) {
-            const R v = fma(FP_EL(z, r), FP_EL(sg, c), fma(FP_EL(sg, r), FP_EL(z, c), get(r, c)));
-            take = take && finite(v);
+            const R h = get(r, c);
+            const R v = fma(FP_EL(z, r), FP_EL(sg, c), fma(FP_EL(sg, r), FP_EL(z, c), h));
+            const R cross = FP_EL(sg, r) * FP_EL(Hy, c) + FP_EL(sg, c) * FP_EL(Hy, r);
+            const R vr = (h - rho * cross) + coef * (FP_EL(sg, r) * FP_EL(sg, c));
+            take = take && finite(v) && finite(vr);
             mx = fabs(v) > mx ? fabs(v) : mx;
           }
         if (take) bound = mx * R(1.0009765625);

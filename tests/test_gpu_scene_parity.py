@@ -137,3 +137,46 @@ def test_order3_random_subsample_against_oracle(city):
     args = (basis[both].astype(f), anchor[both].astype(f), start[both].astype(f), end[both].astype(f))
     assert points_ok(O.path_points(*args, T_dev[both].astype(f))[:, 1:-1],
                      O.path_points(*args, T_ref[both].astype(f))[:, 1:-1]).all()
+
+
+def test_config4_gradient_on_the_real_scene(city):
+    """Config 4 (the inverse-design step) on the real walls scene: loss =
+    sum over valid paths of 1/L^2 and its gradient w.r.t. every wall object
+    (full implicit VJP, cotangent -2/L^3, accumulated on the device), TX and
+    the wall vertices, against the fp64 oracle gradient of every traced
+    valid path (implicit_diff.py:74-106 restated) summed on the host. Within
+    1e-3 relative (the north-star gradient tolerance), norm-wise."""
+    from oracle.cpu_baseline import full_gradient_parallel
+
+    res = trace(city, max_order=3, iterations=20, with_grad=True)
+    N = city.n_objects
+    obj_ref = np.zeros((N, 9))
+    tx_ref = np.zeros(3)
+    loss_ref = 0.0
+    n_paths = 0
+    for o in res.orders:
+        if o.valid == 0:
+            continue
+        seq = o.seq.cpu().numpy()
+        rxi = o.rx.cpu().numpy()
+        T = o.T.cpu().numpy().astype(np.float64)
+        L = o.length.cpu().numpy().astype(np.float64)
+        basis = city.obj_basis[seq].astype(np.float32).astype(np.float64)
+        anchor = city.obj_anchor[seq].astype(np.float32).astype(np.float64)
+        start = np.broadcast_to(city.tx.astype(np.float32).astype(np.float64), (len(seq), 3)).copy()
+        end = city.rx.astype(np.float32).astype(np.float64)[rxi]
+        db, da, d0, d1, ok = full_gradient_parallel(basis, anchor, start, end, T, -2.0 / L ** 3)
+        n_paths += int(ok.sum())
+        loss_ref += float(np.sum(1.0 / L[ok] ** 2))
+        # walls alphabet: reflectors only, every basis element is active
+        np.add.at(obj_ref, seq[ok].ravel(), np.concatenate(
+            [db[ok].reshape(-1, o.order, 6), da[ok]], axis=2).reshape(-1, 9))
+        tx_ref += d0[ok].sum(axis=0)
+    obj = res.obj_grad.cpu().numpy()
+    rel = np.linalg.norm(obj - obj_ref) / np.linalg.norm(obj_ref)
+    print(f"config 4 real scene: {n_paths} valid paths, loss {res.loss:.6e} (oracle {loss_ref:.6e}), "
+          f"object-gradient rel err {rel:.2e}")
+    assert n_paths > 10_000
+    assert res.loss == pytest.approx(loss_ref, rel=1e-4)
+    assert rel <= 1e-3
+    assert np.linalg.norm(res.tx_grad.cpu().numpy() - tx_ref) <= 1e-3 * np.linalg.norm(tx_ref)
