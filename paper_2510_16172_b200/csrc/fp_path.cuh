@@ -280,12 +280,11 @@ struct PathState {
     }
     if (LIGHT) {
       // reciprocal clamped norms of two segments per paired refinement
-      const R eps2 = G.eps * G.eps;
 #pragma unroll
-      for (int m = 0; m < S / 2; ++m) rcp_norm2(qp[m], G.eps, eps2, G.reps, rnp[m]);
+      for (int m = 0; m < S / 2; ++m) rcp_norm2(qp[m], G.eps, G.reps, rnp[m]);
       if constexpr (S & 1) {
         R r;
-        rcp_norm(qp[SP - 1].x, G.eps, eps2, G.reps, r);
+        rcp_norm(qp[SP - 1].x, G.eps, G.reps, r);
         rnp[SP - 1] = mk2(r, R(0));
       }
     } else {
@@ -483,8 +482,9 @@ struct InvHess {
       // the rank-one coefficient times s_i s_j) can overflow in fp32 where
       // the two-term form does not — and then it skips the update
       // (solver.py:196-199). So the update is "suspect" when any of those
-      // magnitudes, or the bound on H', reaches 1e36 (far above every healthy
-      // path, 340x below FLT_MAX); suspect updates evaluate the reference's
+      // magnitudes, or the bound on H', reaches Num<R>::suspect() (1e36 in
+      // fp32: far above every healthy path, 340x below FLT_MAX; 1e305 in
+      // fp64); suspect updates evaluate the reference's
       // expression entry by entry. The magnitudes are FMNMX (ALU pipe)
       // reductions; NaN/inf propagate into `sus` and send the update down
       // the checked path too.
@@ -497,7 +497,7 @@ struct InvHess {
       sus = absmax_nan(sus, smax * (R(4) * half));
       bool take = true;
       uint8_t checked = 0;
-      if (!(sus < R(1e36))) {
+      if (!(sus < Num<R>::suspect())) {
         checked = FP_FATE_ENTRY_CHECK;
         // Rare: possible overflow. Check every entry before committing, in
         // the reference's evaluation order and in the committed form.

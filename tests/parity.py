@@ -64,3 +64,29 @@ def flat_grad(db, da, d0, d1):
 def grad_rel_err(g, g_ref):
     g = np.asarray(g, np.float64)
     return np.linalg.norm(g - g_ref, axis=1) / np.maximum(np.linalg.norm(g_ref, axis=1), 1e-30)
+
+
+def self_agreement(basis, anchor, start, end, T0, iterations, fp_iters, dtype):
+    """The reference's own agreement on its UNCONVERGED paths under a 1-ulp
+    change of the inputs (start nudged to the next representable value):
+    the fraction whose points and lengths stay within the contract
+    tolerance (99.98% RD/10 it, 94.1% RDR/20 it, 90.5%
+    RRR/20 it in fp32). Returns (fraction, count of unconverged paths)."""
+    dt = np.dtype(dtype).type
+    ref = O.solve_outputs(basis, anchor, start, end, T0, iterations, fp_iters, dt)
+    nudged = np.nextafter(np.asarray(start, dt), np.asarray(np.inf, dt))
+    pert = O.solve_outputs(basis, anchor, nudged, end, T0, iterations, fp_iters, dt)
+    conv = converged_mask(basis, anchor, start, end, ref["T"])
+    ok = points_ok(pert["points"], ref["points"]) & lengths_ok(pert["L"], ref["L"])
+    n = int((~conv).sum())
+    return (float(ok[~conv].mean()) if n else 1.0), n
+
+
+def agreement_floor(basis, anchor, start, end, T0, iterations, fp_iters, dtype):
+    """Floor for the GPU's agreement with the reference on unconverged paths:
+    the reference's 1-ulp self-agreement less two binomial standard errors
+    of the sample (and never above 1)."""
+    p, n = self_agreement(basis, anchor, start, end, T0, iterations, fp_iters, dtype)
+    if n == 0:
+        return 0.0
+    return max(0.0, p - 2.0 * np.sqrt(max(p * (1 - p), 1.0 / n) / n))

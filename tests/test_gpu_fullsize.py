@@ -21,7 +21,7 @@ from paper_2510_16172_b200.implicit_diff import vjp_batch
 from paper_2510_16172_b200.solver import Precision, SolveOptions, solve, solve_with_gradients
 from oracle import fermat_oracle as O
 
-from parity import GRAD_REL, converged_mask, flat_grad, grad_rel_err, lengths_ok, points_ok
+from parity import GRAD_REL, agreement_floor, converged_mask, flat_grad, grad_rel_err, lengths_ok, points_ok
 
 pytestmark = pytest.mark.gpu
 
@@ -80,7 +80,8 @@ def test_oracle_subsample_full_size(full):
     conv = converged_mask(*args, ref["T"])
     ok = points_ok(pts, ref["points"]) & lengths_ok(L, ref["L"])
     assert ok[conv].all()
-    assert ok.mean() > 0.8
+    floor = agreement_floor(*args, b.T0[idx], 20, 1, np.float32)
+    assert ok[~conv].mean() >= floor, (ok[~conv].mean(), floor)
     rows = np.nonzero(conv)[0][:256]
     db, da, d0, d1, okg = O.full_gradient_rows(*args, ref["T"], rows)
     got = flat_grad(*(t[it].double().cpu().numpy()[rows] for t in

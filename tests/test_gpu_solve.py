@@ -14,7 +14,8 @@ from paper_2510_16172_b200.batching import BatchScene
 from paper_2510_16172_b200.solver import Precision, SolveOptions, solve
 from oracle import fermat_oracle as O
 
-from parity import GRAD_REL, converged_mask, flat_grad, golden, grad_rel_err, lengths_ok, points_ok
+from parity import (GRAD_REL, agreement_floor, converged_mask, flat_grad, golden, grad_rel_err,
+                    lengths_ok, points_ok)
 
 pytestmark = pytest.mark.gpu
 
@@ -31,6 +32,9 @@ def _solve(d, dtype, iters=None, fp_iters=None, T0=None, **kw):
 
 
 def _check_against(res, T_ref, L_ref, basis, anchor, start, end, min_agree):
+    """Converged paths in tolerance; unconverged ones agree at least as often
+    as the reference agrees with itself under a 1-ulp input change
+    (min_agree: parity.agreement_floor on the same inputs)."""
     T = res.T.cpu().numpy()
     pts = res.points.double().cpu().numpy()
     L = res.length.cpu().numpy()
@@ -42,14 +46,22 @@ def _check_against(res, T_ref, L_ref, basis, anchor, start, end, min_agree):
     assert conv.any()
     assert ok[conv].all(), f"{(~ok[conv]).sum()} converged paths out of tolerance"
     if (~conv).any():
-        assert ok[~conv].mean() >= min_agree, ok[~conv].mean()
+        print(f"unconverged agreement {ok[~conv].mean():.4f} (floor {min_agree:.4f}, {(~conv).sum()} paths)")
+        assert ok[~conv].mean() >= min_agree, (ok[~conv].mean(), min_agree)
     return conv, ok
+
+
+def _floor(d, dt, T0=None, iters=None, fp_iters=None):
+    return agreement_floor(d["basis"], d["anchor"], d["start"], d["end"], d["T0"] if T0 is None else T0,
+                           int(iters if iters is not None else d["iterations"]),
+                           int(fp_iters if fp_iters is not None else d["fp_iters"]), dt)
 
 
 def test_config0_matches_reference():
     d = golden("fwd_config0")
     res = _solve(d, np.float32)
-    conv, ok = _check_against(res, d["T"], d["L"], d["basis"], d["anchor"], d["start"], d["end"], 0.9)
+    conv, ok = _check_against(res, d["T"], d["L"], d["basis"], d["anchor"], d["start"], d["end"],
+                              _floor(d, np.float32))
     # device gate agrees with the oracle classification on the clear cases
     dev_conv = res.converged.cpu().numpy()
     assert (dev_conv[conv]).mean() > 0.99
@@ -59,14 +71,16 @@ def test_config0_matches_reference():
 def test_mixed_orderings_fp32(K):
     d = golden(f"fwd_mixed_k{K}")
     res = _solve(d, np.float32)
-    _check_against(res, d["T_f32"], d["L_f32"], d["basis"], d["anchor"], d["start"], d["end"], 0.8)
+    _check_against(res, d["T_f32"], d["L_f32"], d["basis"], d["anchor"], d["start"], d["end"],
+                   _floor(d, np.float32))
 
 
 @pytest.mark.parametrize("K", [1, 2, 3, 4, 5])
 def test_mixed_orderings_fp64(K):
     d = golden(f"fwd_mixed_k{K}")
     res = _solve(d, np.float64)
-    _check_against(res, d["T_f64"], d["L_f64"], d["basis"], d["anchor"], d["start"], d["end"], 0.9)
+    _check_against(res, d["T_f64"], d["L_f64"], d["basis"], d["anchor"], d["start"], d["end"],
+                   _floor(d, np.float64))
     # fp64 on converged paths is far tighter than the fp32 contract
     conv = converged_mask(d["basis"], d["anchor"], d["start"], d["end"], d["T_f64"])
     T = res.T.cpu().numpy()
@@ -82,7 +96,7 @@ def test_reference_generator_scenes(kinds, n):
         res = _solve(d, dt)
         T = res.T.cpu().numpy()
         _check_against(res, d["T" + suf], d["L" + suf], d["basis"], d["anchor"], d["start"],
-                       d["end"], 0.9)
+                       d["end"], _floor(d, dt))
         if kinds == "diffractions":
             # inert coordinates come back bitwise untouched (test_acceptance.py:120-134)
             assert np.array_equal(T[..., 1], d["T0"][..., 1].astype(dt))

@@ -276,7 +276,11 @@ def test_near_singular_solve_follows_the_reference_fallback():
     block solve applies _solve_sym's residual check and Tikhonov retry
     (implicit_diff.py:55-71), so u follows the reference on both sides of
     the trigger. Tolerance: the conditioning-limited accuracy of any fp64
-    solve, 1e-15 cond (>= 1e-10), relative."""
+    solve, 1e-15 cond (>= 1e-10), relative — except where the reference's
+    own LAPACK residual lies within a factor 20 of the 1e-8 (1 + |rhs|)
+    bound: there the verdict is decided by rounding (any other fp64
+    arithmetic may land on the other side), and either outcome is accepted,
+    i.e. the Tikhonov shift's effect lambda / lambda_min ~ 1e-12 cond."""
     d = golden("near_singular_k1")
     sc = BatchScene(d["basis"], d["anchor"], d["start"], d["end"]).astype(np.float64)
     g, st, u = vjp_batch(sc, torch.from_numpy(d["T"]).cuda(), v_T=torch.from_numpy(d["v"]).cuda(),
@@ -285,7 +289,12 @@ def test_near_singular_solve_follows_the_reference_fallback():
     assert not (st.cpu().numpy() & _lib.STATUS_SINGULAR).any()
     for j in range(len(u)):
         H = O.scalar_hessian(d["basis"][j], d["anchor"][j], d["start"][j], d["end"][j], d["T"][j])
-        tol = max(1e-10, 1e-15 * np.linalg.cond(H))
+        cond = np.linalg.cond(H)
+        rhs = -d["v"][j].ravel()
+        ratio = np.linalg.norm(H @ np.linalg.solve(H, rhs) - rhs) / (1e-8 * (1 + np.linalg.norm(rhs)))
+        tol = max(1e-10, 1e-15 * cond)
+        if 0.05 < ratio < 20:
+            tol = max(tol, 2e-12 * cond)
         rel = np.linalg.norm(u[j] - d["u"][j]) / np.linalg.norm(d["u"][j])
         assert rel <= tol, (j, rel, tol, bool(d["fired"][j]))
         got = flat_grad(*(t.cpu().numpy()[j:j + 1] for t in (g.basis, g.anchor, g.start, g.end)))
