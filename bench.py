@@ -435,7 +435,8 @@ def run_ours(args):
     # FP32 roofline probe first: it also brings the SM clock up from idle
     # before the warm-up steps, so the first timed steps are not ramping.
     peak = measure_ffma_peak(lib, stream, dev) if rank == 0 else None
-    peak_reg = measure_ffma_peak(lib, stream, dev, register_operands=True) if rank == 0 else None
+    peak_reg = (measure_ffma_peak(lib, stream, dev, register_operands=True)
+                if rank == 0 and hasattr(lib, "fp_peak_ffma_reg") else None)
 
     # ---- fused forward + VJP step (the headline) ------------------------------
     sampler = ClockSampler(torch.cuda.current_device())
