@@ -69,6 +69,53 @@ __device__ __forceinline__ double2 add2(double2 a, double2 b) { return make_doub
 __device__ __forceinline__ double2 neg2(double2 a) { return make_double2(-a.x, -a.y); }
 __device__ __forceinline__ double2 sub2(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 
+// Pair ops on the last pair of an odd-length vector (`lo` true: its high lane
+// is padding, never read): one scalar op on the low lane instead of the
+// pair — half the FMA-pipe cycles, identical low-lane rounding; the high
+// lane of the result is left undefined. `lo` is a compile-time constant
+// after unrolling.
+__device__ __forceinline__ float2 lo_only(float x) {
+  float2 r;
+  r.x = x;
+  return r;
+}
+__device__ __forceinline__ double2 lo_only(double x) {
+  double2 r;
+  r.x = x;
+  return r;
+}
+// (`lo` must be a genuine bool: an array or pointer would convert silently)
+template <typename B, typename P>
+__device__ __forceinline__ P fma2p(B lo, P a, P b, P c) {
+  static_assert(std::is_same<B, bool>::value, "lo must be a bool");
+  return lo ? lo_only(fma(a.x, b.x, c.x)) : fma2(a, b, c);
+}
+template <typename B, typename P>
+__device__ __forceinline__ P mul2p(B lo, P a, P b) {
+  static_assert(std::is_same<B, bool>::value, "lo must be a bool");
+  return lo ? lo_only(a.x * b.x) : mul2(a, b);
+}
+template <typename B, typename P, typename R>
+__device__ __forceinline__ P mulzp(B lo, P a, P b, R nz) {
+  static_assert(std::is_same<B, bool>::value, "lo must be a bool");
+  return lo ? lo_only(a.x * b.x) : mulz(a, b, nz);
+}
+template <typename B, typename P>
+__device__ __forceinline__ P add2p(B lo, P a, P b) {
+  static_assert(std::is_same<B, bool>::value, "lo must be a bool");
+  return lo ? lo_only(a.x + b.x) : add2(a, b);
+}
+template <typename B, typename P>
+__device__ __forceinline__ P sub2p(B lo, P a, P b) {
+  static_assert(std::is_same<B, bool>::value, "lo must be a bool");
+  return lo ? lo_only(a.x - b.x) : sub2(a, b);
+}
+template <typename B, typename P>
+__device__ __forceinline__ P neg2p(B lo, P a) {
+  static_assert(std::is_same<B, bool>::value, "lo must be a bool");
+  return lo ? lo_only(-a.x) : neg2(a);
+}
+
 // Lane access by value / by store (never a reference picked by a condition:
 // a selected pointer into the pair defeats scalar replacement and sends the
 // whole state to local memory in the large tile kernels).
@@ -285,7 +332,7 @@ struct PathState {
       if constexpr (S & 1) {
         R r;
         rcp_norm(qp[SP - 1].x, G.eps, G.reps, r);
-        rnp[SP - 1] = mk2(r, R(0));
+        rnp[SP - 1].x = r;  // high lane: padding, never read
       }
     } else {
 #pragma unroll
@@ -294,14 +341,12 @@ struct PathState {
         norm_rcp(FP_EL(qp, k), G.eps, G.reps, nu[k], nc, r);
         FP_SET(rnp, k, r);
       }
-      if constexpr (S & 1) rnp[SP - 1].y = R(0);
     }
 #pragma unroll
     for (int k = 0; k < S; ++k) {
       uxy[k] = mulz(sxy[k], bc2(RN(k)), G.nz);
       uz[k] = sz[k] * RN(k);
     }
-    if constexpr (NA & 1) gout[NP - 1].y = R(0);
 #pragma unroll
     for (int i = 0; i < K; ++i) {
       const V2<R> qxy = sub2(uxy[i], uxy[i + 1]);
@@ -432,9 +477,10 @@ struct InvHess {
   __device__ __forceinline__ void mul(const V2<R> (&v)[NP], V2<R> (&out)[NP], R nz) const {
 #pragma unroll
     for (int m = 0; m < NP; ++m) {
+      const bool pad = (NA & 1) && m == NP - 1;  // padding high lane
       V2<R> acc;
       if (m == 0) {
-        acc = NA > 1 ? mul2(h[pid(0, 0)], bc2(v[0].x)) : mulz(h[pid(0, 0)], bc2(v[0].x), nz);
+        acc = NA > 1 ? mul2(h[pid(0, 0)], bc2(v[0].x)) : mulzp(pad, h[pid(0, 0)], bc2(v[0].x), nz);
       } else {
         R lo[2];
 #pragma unroll
@@ -449,7 +495,7 @@ struct InvHess {
           for (int mm = 1; mm < m; ++mm) l = fma2(h[pid(mm, c)], v[mm], l);
           lo[e] = l.x + l.y;
         }
-        acc = fma2(h[pid(m, 2 * m)], bc2(v[m].x), mk2(lo[0], lo[1]));
+        acc = fma2p(pad, h[pid(m, 2 * m)], bc2(v[m].x), mk2(lo[0], lo[1]));
       }
 #pragma unroll
       for (int c = 2 * m + 1; c < NA; ++c) acc = fma2(h[pid(m, c)], bc2(FP_EL(v, c)), acc);
@@ -469,14 +515,17 @@ struct InvHess {
     if (ok) {
       V2<R> Hy[NP];
 #pragma unroll
-      for (int m = 0; m < NP; ++m) Hy[m] = add2(Hg[m], p[m]);
+      for (int m = 0; m < NP; ++m) Hy[m] = add2p((NA & 1) && m == NP - 1, Hg[m], p[m]);
       const R rho = rcp_fast(sy);
       const R yHy = dotv<R, NA>(y, Hy, nz);
       const R rr = rho * rho;
       const R half = R(0.5) * fma(rr, yHy, rho);
       V2<R> z[NP];
 #pragma unroll
-      for (int m = 0; m < NP; ++m) z[m] = fma2(bc2(half), sg[m], mul2(bc2(-rho), Hy[m]));
+      for (int m = 0; m < NP; ++m) {
+        const bool lo = (NA & 1) && m == NP - 1;
+        z[m] = fma2p(lo, bc2(half), sg[m], mul2p(lo, bc2(-rho), Hy[m]));
+      }
       // |H'_ij| <= bound + |z_i s_j + s_i z_j| <= bound + 2 max|s| max|z|, and
       // |z_j| <= |half| max|s| + rho max|Hy|, so w = max|s| (|half| max|s| +
       // rho max|Hy|) bounds |s_i z_j| — and also the reference's products
@@ -524,21 +573,26 @@ struct InvHess {
 #pragma unroll
         for (int m = 0; m < NP; ++m) {
 #pragma unroll
-          for (int c = 2 * m; c < NA; ++c)
-            h[pid(m, c)] = fma2(z[m], bc2(FP_EL(sg, c)), fma2(sg[m], bc2(FP_EL(z, c)), h[pid(m, c)]));
+          for (int c = 2 * m; c < NA; ++c) {
+            const bool lo = (NA & 1) && m == NP - 1;  // the padded diagonal pair
+            h[pid(m, c)] = fma2p(lo, z[m], bc2(FP_EL(sg, c)), fma2p(lo, sg[m], bc2(FP_EL(z, c)), h[pid(m, c)]));
+          }
           if (2 * m + 1 < NA) h[pid(m, 2 * m)].y = h[pid(m, 2 * m + 1)].x;  // keep H symmetric
         }
         const R zg = dotv<R, NA>(z, gn, nz), sgn = dotv<R, NA>(sg, gn, nz);
 #pragma unroll
-        for (int m = 0; m < NP; ++m) p[m] = fma2(sg[m], bc2(-zg), fma2(z[m], bc2(-sgn), neg2(Hg[m])));
+        for (int m = 0; m < NP; ++m) {
+          const bool lo = (NA & 1) && m == NP - 1;
+          p[m] = fma2p(lo, sg[m], bc2(-zg), fma2p(lo, z[m], bc2(-sgn), neg2p(lo, Hg[m])));
+        }
         return checked;
       }
 #pragma unroll
-      for (int m = 0; m < NP; ++m) p[m] = neg2(Hg[m]);
+      for (int m = 0; m < NP; ++m) p[m] = neg2p((NA & 1) && m == NP - 1, Hg[m]);
       return FP_FATE_NONFINITE_SKIP | checked;
     }
 #pragma unroll
-    for (int m = 0; m < NP; ++m) p[m] = neg2(Hg[m]);
+    for (int m = 0; m < NP; ++m) p[m] = neg2p((NA & 1) && m == NP - 1, Hg[m]);
     return FP_FATE_CURVATURE_SKIP;
   }
 };
@@ -581,14 +635,15 @@ __device__ __forceinline__ void bfgs_iterations(const Geo<R, K>& G, PathState<R,
     V2<R> sg[NP];
 #pragma unroll
     for (int m = 0; m < NP; ++m) {
-      sg[m] = mulz(bc2(alpha), p[m], G.nz);
-      P.t[m] = add2(P.t[m], sg[m]);
+      const bool lo = (NA & 1) && m == NP - 1;  // padding high lane
+      sg[m] = mulzp(lo, bc2(alpha), p[m], G.nz);
+      P.t[m] = add2p(lo, P.t[m], sg[m]);
     }
     V2<R> gn[NP];
     P.template eval<true>(G, gn);
     V2<R> y[NP];
 #pragma unroll
-    for (int m = 0; m < NP; ++m) y[m] = sub2(gn[m], P.g[m]);
+    for (int m = 0; m < NP; ++m) y[m] = sub2p((NA & 1) && m == NP - 1, gn[m], P.g[m]);
     // Curvature test sy > 1e-12 |s| |y| (solver.py:184), branch-free: with
     // paired dot products the two norms cost less than the register moves a
     // rarely-taken branch forces on the hot path.

@@ -301,3 +301,22 @@ def test_tile_and_bucketed_dispatch_bitwise_equal(K, layout, prec):
                      (grads.start, ref_g.start), (grads.end, ref_g.end), (fwd.T, ref_f.T),
                      (fwd.g, ref_f.g), (fwd.points, ref_f.points), (fwd.status, ref_f.status)):
             assert torch.equal(x, y), pol
+
+
+@pytest.mark.parametrize("prec", [Precision.SINGLE, Precision.DOUBLE])
+def test_repeat_runs_bitwise_identical(prec):
+    """Every order 1..8: two runs of the fused step on the same inputs return
+    the same bits in every output (no read of an undefined register lane or
+    of stale shared memory can go unnoticed)."""
+    from paper_2510_16172_b200.solver import solve_with_gradients
+
+    for K in range(1, 9):
+        orders = datagen.all_orderings(K) if K <= 5 else datagen.all_orderings(K)[:8]
+        b = datagen.gen_batch(700 + K, orders, 4096 // len(orders))
+        sc = BatchScene(b.basis, b.anchor, b.start, b.end)
+        opts = SolveOptions(iterations=20, precision=prec)
+        runs = [solve_with_gradients(sc, b.T0, opts) for _ in range(2)]
+        (r1, g1), (r2, g2) = runs
+        for x, y in ((r1.T, r2.T), (r1.length, r2.length), (r1.status, r2.status), (r1.points, r2.points),
+                     (g1.basis, g2.basis), (g1.anchor, g2.anchor), (g1.start, g2.start), (g1.end, g2.end)):
+            assert torch.equal(x.view(torch.uint8), y.view(torch.uint8)), K
