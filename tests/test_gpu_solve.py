@@ -188,6 +188,14 @@ def test_edge_cases_empty_order0_and_errors():
     sc0 = BatchScene(np.zeros((2, 0, 3, 2)), np.zeros((2, 0, 3)), x0, x1)
     r0 = solve(sc0, None, SolveOptions(iterations=3))
     assert np.allclose(r0.length.cpu().numpy(), [5.0, 1.0])
+    # order 0 with record_trace: empty per-path traces like the reference
+    # (solver.py:160-164), also through the scalar grad_tol early stop
+    from paper_2510_16172_b200.solver import _bfgs_kernel
+    T, g, traces = _bfgs_kernel(sc0, np.zeros((2, 0, 2)), SolveOptions(iterations=3, record_trace=True))
+    assert T.shape == (2, 0, 2) and g.shape == (2, 0, 2) and traces == [[], []]
+    spec0 = fp.PathSpec(start=x0[0], end=x1[0], surfaces=())
+    rep = fp.bfgs_solve(spec0, np.zeros((0, 2)), SolveOptions(iterations=3, record_trace=True, grad_tol=1e-6))
+    assert rep.trace == [] and rep.final_length == pytest.approx(5.0)
     big = datagen.gen_batch(1, ["R" * 65], 4)  # above MAX_INTERACTIONS (geometry.py:23)
     with pytest.raises(NotImplementedError):
         solve(BatchScene(big.basis, big.anchor, big.start, big.end), big.T0, SolveOptions(iterations=2))
