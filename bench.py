@@ -129,6 +129,9 @@ def _init_dist(args):
         import torch.distributed as dist
 
         if args.backend == "nccl":
+            # the communicator's init line (stderr) reports nranks = N
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group("gloo")
