@@ -614,6 +614,11 @@ __device__ __forceinline__ bool stationary(const V2<R> (&g)[Packed<NA>::NP], R l
   return Num<R>::sqrt_(norm2_seq<R, NA>(g)) < R(1e-5) * (R(1) + len);
 }
 
+#ifndef FP_UNROLL_MAX_K
+#define FP_UNROLL_MAX_K 1
+#endif
+constexpr int kUnrollMaxOrder = FP_UNROLL_MAX_K;
+
 // The BFGS iterations (solver.py:171-211). GENERAL = false is the common case
 // compiled without the per-iteration checks: one fixed-point step (F = 1, the
 // reference default solver.py:45) and no trace.
@@ -628,6 +633,10 @@ __device__ __forceinline__ void bfgs_iterations(const Geo<R, K>& G, PathState<R,
   constexpr int NA = L::NA;
   constexpr int NP = Packed<NA>::NP;
   const int fp_iters = GENERAL ? fp_iters_rt : 1;
+  // Short loop bodies (order 1) run two iterations per trip: -1.2% at K=1
+  // (tools/ab_libs.sh; at K=3 unrolling measured slower, instruction cache).
+  constexpr int kUnroll = (K <= kUnrollMaxOrder && !GENERAL) ? 2 : 1;
+#pragma unroll(kUnroll)
   for (int it = 0; it < iterations; ++it) {
     bool zero;
     const R alpha = P.step_size(G, p, fp_iters, zero);
