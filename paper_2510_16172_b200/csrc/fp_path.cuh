@@ -326,12 +326,13 @@ struct PathState {
       FP_SET(qp, k, fma(sz[k], sz[k], q));
     }
     if (LIGHT) {
-      // reciprocal clamped norms of two segments per paired refinement
+      // reciprocal clamped norms (MUFU.RSQ, fp_common.cuh rcp_norm)
+      const R eps2 = G.eps * G.eps;
 #pragma unroll
-      for (int m = 0; m < S / 2; ++m) rcp_norm2(qp[m], G.eps, G.reps, rnp[m]);
+      for (int m = 0; m < S / 2; ++m) rcp_norm2(qp[m], G.eps, eps2, G.reps, rnp[m]);
       if constexpr (S & 1) {
         R r;
-        rcp_norm(qp[SP - 1].x, G.eps, G.reps, r);
+        rcp_norm(qp[SP - 1].x, G.eps, eps2, G.reps, r);
         rnp[SP - 1].x = r;  // high lane: padding, never read
       }
     } else {

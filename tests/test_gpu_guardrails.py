@@ -23,10 +23,7 @@ exercise each branch:
 
 Fates are compared on DECISIVE updates — while the path is still far from
 converged — because past convergence s and y are rounding noise and the
-curvature test is a coin toss in any arithmetic. (Known divergence, not
-tested: segments longer than 1.8e19 m overflow |s|^2 in fp32; the reference
-then divides by an infinite norm and keeps going, the kernels' refined
-reciprocal square root turns it into NaN — both report a non-finite length.)
+curvature test is a coin toss in any arithmetic.
 """
 
 import numpy as np
