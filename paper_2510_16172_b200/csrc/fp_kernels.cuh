@@ -217,7 +217,7 @@ __device__ __forceinline__ void run_path(const PathArgs<R>& a, int64_t row, cons
     tin[i] = in.T[2 * i + 1];
   }
   uint8_t st = 0;
-  P.eval(G, P.g);
+  P.eval_entry(G);
   if (OP != OP_VJP)
     st |= bfgs_solve<R, K, MASK>(G, P, a.iterations, a.fp_iters, a.trace_len, a.trace_gnorm,
                                  a.trace_fate, a.ld, row, a.H_out);
