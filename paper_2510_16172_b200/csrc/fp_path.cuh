@@ -663,14 +663,29 @@ __device__ __forceinline__ void bfgs_iterations(const Geo<R, K>& G, PathState<R,
     V2<R> y[NP];
 #pragma unroll
     for (int m = 0; m < NP; ++m) y[m] = sub2p((NA & 1) && m == NP - 1, gn[m], P.g[m]);
-    // Curvature test sy > 1e-12 |s| |y| (solver.py:184), branch-free: with
-    // paired dot products the two norms cost less than the register moves a
-    // rarely-taken branch forces on the hot path.
+    // Curvature test sy > 1e-12 |s| |y| (solver.py:184). From 3 unknowns on,
+    // the norms come only when needed: |s| |y| <= NA max|s| max|y| (FMNMX
+    // reductions, ALU pipe), so above that bound the test passes and at or
+    // below 0 it fails — the same verdicts, bit for bit; only the band in
+    // between (s, y nearly orthogonal) evaluates the norms (K=3 fused -0.7%,
+    // forward -1.3%, K=2 -1.1%; slower for 1-2 unknowns, which keep the
+    // branch-free dots).
     const R sy = dotv<R, NA>(sg, y, G.nz);
-    const R ss = dotv<R, NA>(sg, sg, G.nz);
-    const R yy = dotv<R, NA>(y, y, G.nz);
-    const bool ok = sy > (R(1e-12) * sqrt_test(ss)) * sqrt_test(yy);
     const R ms = absmaxv<R, NA>(sg);
+    bool ok;
+    if constexpr (NA >= 3) {
+      const R my = absmaxv<R, NA>(y);
+      ok = sy > (R(1e-12 * NA * 1.0001) * ms) * my;
+      if (!ok && sy > R(0)) {
+        const R ss = dotv<R, NA>(sg, sg, G.nz);
+        const R yy = dotv<R, NA>(y, y, G.nz);
+        ok = sy > (R(1e-12) * sqrt_test(ss)) * sqrt_test(yy);
+      }
+    } else {
+      const R ss = dotv<R, NA>(sg, sg, G.nz);
+      const R yy = dotv<R, NA>(y, y, G.nz);
+      ok = sy > (R(1e-12) * sqrt_test(ss)) * sqrt_test(yy);
+    }
     const uint8_t fate = H.step(sg, y, gn, p, ok, sy, ms, G.nz);
 #pragma unroll
     for (int m = 0; m < NP; ++m) P.g[m] = gn[m];
