@@ -668,14 +668,16 @@ __device__ __forceinline__ void bfgs_iterations(const Geo<R, K>& G, PathState<R,
     // reductions, ALU pipe), so above that bound the test passes and at or
     // below 0 it fails — the same verdicts, bit for bit; only the band in
     // between (s, y nearly orthogonal) evaluates the norms (K=3 fused -0.7%,
-    // forward -1.3%, K=2 -1.1%; slower for 1-2 unknowns, which keep the
-    // branch-free dots).
+    // forward -1.3%, K=2 -1.1%; slower for 1-2 unknowns and for the
+    // out-of-line variants of orders 4-5, which keep the branch-free dots).
     const R sy = dotv<R, NA>(sg, y, G.nz);
     const R ms = absmaxv<R, NA>(sg);
     bool ok;
-    if constexpr (NA >= 3) {
+    if constexpr (NA >= 3 && K <= 3) {
+      // (while |s|^2 and |y|^2 cannot overflow: past that the reference's
+      // norms are infinite and its test fails, which the exact path follows)
       const R my = absmaxv<R, NA>(y);
-      ok = sy > (R(1e-12 * NA * 1.0001) * ms) * my;
+      ok = absmax_nan(ms, my) < Num<R>::sqrt_big() && sy > (R(1e-12 * NA * 1.0001) * ms) * my;
       if (!ok && sy > R(0)) {
         const R ss = dotv<R, NA>(sg, sg, G.nz);
         const R yy = dotv<R, NA>(y, y, G.nz);
