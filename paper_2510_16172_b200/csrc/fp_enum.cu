@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(kThreads, (MinBlocks<float, Lay<K, MASK>::NA>:
       load_geo<float, K, MASK>(G, bb, aa, x0, x1);
       G.nz = a.nz;
       P.zero_t();
-      P.eval_entry(G);
+      P.eval(G, P.g);
       uint8_t st = bfgs_solve<float, K, MASK>(G, P, a.iterations, a.fp_iters, nullptr, nullptr, nullptr, 0, 0,
                                               nullptr);
       st |= final_status<float, K, MASK>(G, P);

@@ -217,7 +217,13 @@ __device__ __forceinline__ void run_path(const PathArgs<R>& a, int64_t row, cons
     tin[i] = in.T[2 * i + 1];
   }
   uint8_t st = 0;
-  P.eval_entry(G);
+  // The solve starts from the refined evaluation; the VJP-only op evaluates
+  // T* the way the loop's last iteration did (eval_entry), so a fused step
+  // and solve-then-VJP agree bit for bit.
+  if (OP == OP_VJP)
+    P.eval_entry(G);
+  else
+    P.eval(G, P.g);
   if (OP != OP_VJP)
     st |= bfgs_solve<R, K, MASK>(G, P, a.iterations, a.fp_iters, a.trace_len, a.trace_gnorm,
                                  a.trace_fate, a.ld, row, a.H_out);

@@ -358,10 +358,10 @@ struct PathState {
     }
   }
 
-  // Evaluation at the starting parameters (and at T* for the VJP-only op):
-  // the loop's reciprocal norms and gradient (eval<true>), then the
-  // unclamped norms. Every op evaluates a path the same way, so the fused
-  // step, solve-then-VJP and VJP-only agree bit for bit.
+  // Evaluation at T* for the VJP-only op: the loop's reciprocal norms and
+  // gradient (eval<true>), then the unclamped norms — the state a solve
+  // ends in, so the fused step, solve-then-VJP and VJP-only agree bit for
+  // bit.
   __device__ __forceinline__ void eval_entry(const Geo<R, K>& G) {
     eval<true>(G, g);
     finish_norms(G);
