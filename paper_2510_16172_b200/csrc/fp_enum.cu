@@ -65,8 +65,19 @@ __device__ __forceinline__ void decode(const EnumArgs& a, int64_t c, int& rx, in
   }
 }
 
+// Register budget: the path kernels' NA rule; FP_ENUM_MIN_BLOCKS overrides
+// (A/B builds).
+template <int NA>
+struct EnumMinBlocks {
+#ifdef FP_ENUM_MIN_BLOCKS
+  static constexpr int value = FP_ENUM_MIN_BLOCKS;
+#else
+  static constexpr int value = MinBlocks<float, NA>::value;
+#endif
+};
+
 template <int K, unsigned MASK, bool GRAD>
-__global__ void __launch_bounds__(kThreads, (MinBlocks<float, Lay<K, MASK>::NA>::value))
+__global__ void __launch_bounds__(kThreads, (EnumMinBlocks<Lay<K, MASK>::NA>::value))
     enum_kernel(const EnumArgs a) {
   using L = Lay<K, MASK>;
   constexpr int NA = L::NA;
