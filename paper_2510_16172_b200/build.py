@@ -80,7 +80,10 @@ def _units(orders=ORDERS, obj_dir=None):
 
 def _compile(unit, extra=()):
     src, obj, defs = unit
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *extra, *defs, "-c", src, "-o", obj]
+    flags = NVCC_FLAGS
+    if "-DFP_FMAD" in extra:  # A/B builds only: let nvcc contract mul + add
+        flags = ["-fmad=true" if f == "-fmad=false" else f for f in flags]
+    cmd = [nvcc(), *ARCH, *flags, *extra, *defs, "-c", src, "-o", obj]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed for {os.path.basename(obj)}:\n{res.stderr}")
