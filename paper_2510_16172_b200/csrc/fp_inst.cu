@@ -63,10 +63,18 @@ cudaError_t dispatch_masked_solve_vjp<kK>(const PathArgs<float>& a, unsigned mas
   return by_mask<OP_SOLVE_VJP, 0u>(mask, a, s);
 }
 #elif FP_INST_PART == 3
+// fp32 tile kernels. Orders <= FP_PAIR_MAX_K would run two paths per thread
+// (fp_pair.cuh): bitwise the same results, but measured slower (K=1 0.466 vs
+// 0.411 ms, K=2 0.95 vs 0.72 ms: half the warps per SM for the same
+// dependency chains; profiles/r02s_ab_pair.txt), so 0 (off) by default.
+#ifndef FP_PAIR_MAX_K
+#define FP_PAIR_MAX_K 0
+#endif
 template <>
 cudaError_t dispatch_tile<float, kK>(const PathArgs<float>& a, int op, cudaStream_t s) {
-  return op == OP_SOLVE_VJP ? launch_path_impl<float, kK, kAnyMask, OP_SOLVE_VJP>(a, s)
-                            : launch_path_impl<float, kK, kAnyMask, OP_SOLVE>(a, s);
+  constexpr bool kPair = kK <= FP_PAIR_MAX_K;
+  return op == OP_SOLVE_VJP ? launch_path_impl<float, kK, kAnyMask, OP_SOLVE_VJP, kPair>(a, s)
+                            : launch_path_impl<float, kK, kAnyMask, OP_SOLVE, kPair>(a, s);
 }
 #elif FP_INST_PART == 4
 template <>

@@ -12,6 +12,7 @@
 
 #include <atomic>
 
+#include "fp_pair.cuh"
 #include "fp_path.cuh"
 
 namespace fp {
@@ -199,16 +200,16 @@ __device__ __forceinline__ void load_rec(Rec<R, K>& r, const R* b, const R* a, c
 }
 
 // ---- the per-path body -------------------------------------------------------
+// Stage 1: geometry, the initial unknowns and their evaluation. The solve
+// starts from the refined evaluation; the VJP-only op evaluates T* the way
+// the loop's last iteration did (eval_entry), so a fused step and
+// solve-then-VJP agree bit for bit.
 template <typename R, int K, unsigned MASK, int OP>
-__device__ __forceinline__ void run_path(const PathArgs<R>& a, int64_t row, const Rec<R, K>& in,
-                                         bool has_v, int tid, bool staged, unsigned char* slab) {
+__device__ __forceinline__ void begin_path(const PathArgs<R>& a, const Rec<R, K>& in, Geo<R, K>& G,
+                                           PathState<R, K, MASK>& P, R (&tin)[K]) {
   using L = Lay<K, MASK>;
-  constexpr int NA = L::NA;
-  Geo<R, K> G;
   load_geo<R, K, MASK>(G, in.b, in.a, in.x0, in.x1);
   G.nz = a.nz;
-  PathState<R, K, MASK> P;
-  R tin[K];
   P.zero_t();
 #pragma unroll
   for (int i = 0; i < K; ++i) {
@@ -216,17 +217,20 @@ __device__ __forceinline__ void run_path(const PathArgs<R>& a, int64_t row, cons
     if (L::plane(i)) P.setT(L::idx(i, 1), in.T[2 * i + 1]);
     tin[i] = in.T[2 * i + 1];
   }
-  uint8_t st = 0;
-  // The solve starts from the refined evaluation; the VJP-only op evaluates
-  // T* the way the loop's last iteration did (eval_entry), so a fused step
-  // and solve-then-VJP agree bit for bit.
   if (OP == OP_VJP)
     P.eval_entry(G);
   else
     P.eval(G, P.g);
-  if (OP != OP_VJP)
-    st |= bfgs_solve<R, K, MASK>(G, P, a.iterations, a.fp_iters, a.trace_len, a.trace_gnorm,
-                                 a.trace_fate, a.ld, row, a.H_out);
+}
+
+// Stage 3: classification at the returned T, outputs and (VJP ops) the
+// implicit VJP.
+template <typename R, int K, unsigned MASK, int OP>
+__device__ __forceinline__ void finish_path(const PathArgs<R>& a, int64_t row, const Rec<R, K>& in,
+                                            bool has_v, int tid, bool staged, unsigned char* slab,
+                                            const Geo<R, K>& G, const PathState<R, K, MASK>& P,
+                                            const R (&tin)[K], uint8_t st) {
+  using L = Lay<K, MASK>;
   st |= final_status<R, K, MASK>(G, P);
   bool fin = (st & FP_STATUS_NONFINITE) == 0;
 
@@ -300,6 +304,50 @@ __device__ __forceinline__ void run_path(const PathArgs<R>& a, int64_t row, cons
   if (o.st) o.st[0] = st;
 }
 
+template <typename R, int K, unsigned MASK, int OP>
+__device__ __forceinline__ void run_path(const PathArgs<R>& a, int64_t row, const Rec<R, K>& in,
+                                         bool has_v, int tid, bool staged, unsigned char* slab) {
+  Geo<R, K> G;
+  PathState<R, K, MASK> P;
+  R tin[K];
+  begin_path<R, K, MASK, OP>(a, in, G, P, tin);
+  uint8_t st = 0;
+  if (OP != OP_VJP)
+    st |= bfgs_solve<R, K, MASK>(G, P, a.iterations, a.fp_iters, a.trace_len, a.trace_gnorm,
+                                 a.trace_fate, a.ld, row, a.H_out);
+  finish_path<R, K, MASK, OP>(a, row, in, has_v, tid, staged, slab, G, P, tin, st);
+}
+
+// Two paths of the same kind mask through the paired loop (fp_pair.cuh):
+// stages 1 and 3 per path, the BFGS iterations for both at once. Only the
+// loop's common form (F = 1, no trace, no final H): the caller checks.
+template <int K, unsigned MASK, int OP>
+__device__ __forceinline__ void run_pair(const PathArgs<float>& a, int64_t rowa, int64_t rowb,
+                                         const Rec<float, K>& ina, const Rec<float, K>& inb,
+                                         bool has_v, int tida, int tidb, unsigned char* slab) {
+  static_assert(OP != OP_VJP, "the VJP-only op has no loop");
+  Geo<float, K> ga, gb;
+  PathState<float, K, MASK> pa, pb;
+  float tina[K], tinb[K];
+  begin_path<float, K, MASK, OP>(a, ina, ga, pa, tina);
+  begin_path<float, K, MASK, OP>(a, inb, gb, pb, tinb);
+  // checked_segments (bfgs_solve)
+  uint8_t sta = pa.min_norm() <= ga.eps ? FP_STATUS_DEGENERATE_ENTRY : 0;
+  uint8_t stb = pb.min_norm() <= gb.eps ? FP_STATUS_DEGENERATE_ENTRY : 0;
+  {
+    GeoX<K> G;
+    PairState<K, MASK> P;
+    pack_pair<K, MASK>(ga, gb, pa, pb, G, P);
+    bfgs_pair<K, MASK>(G, P, a.iterations, sta, stb);
+    unpack_lane<K, MASK>(P, 0, pa);
+    unpack_lane<K, MASK>(P, 1, pb);
+  }
+  pa.finish_norms(ga);
+  pb.finish_norms(gb);
+  finish_path<float, K, MASK, OP>(a, rowa, ina, has_v, tida, true, slab, ga, pa, tina, sta);
+  finish_path<float, K, MASK, OP>(a, rowb, inb, has_v, tidb, true, slab, gb, pb, tinb, stb);
+}
+
 // ---- per-warp kind-mask dispatch (the "tile" kernels) -------------------------
 // MASK == kAnyMask instantiates path_kernel with every specialised variant of
 // order K inlined: each thread derives its path's kind mask from the staged
@@ -344,6 +392,19 @@ __device__ __forceinline__ void run_any_mask(unsigned m, const PathArgs<R>& a, i
   if constexpr (M + 1 < (1u << K)) run_any_mask<R, K, OP, M + 1>(m, a, row, in, has_v, tid, slab);
 }
 
+template <int K, int OP, unsigned M = 0>
+__device__ __forceinline__ void run_pair_any_mask(unsigned m, const PathArgs<float>& a, int64_t rowa,
+                                                  int64_t rowb, const Rec<float, K>& ina,
+                                                  const Rec<float, K>& inb, bool has_v, int tida,
+                                                  int tidb, unsigned char* slab) {
+  if (m == M) {
+    run_pair<K, M, OP>(a, rowa, rowb, ina, inb, has_v, tida, tidb, slab);
+    return;
+  }
+  if constexpr (M + 1 < (1u << K))
+    run_pair_any_mask<K, OP, M + 1>(m, a, rowa, rowb, ina, inb, has_v, tida, tidb, slab);
+}
+
 // Copy `width`-element records of the tile from global to shared memory with
 // asynchronous copies (cp.async, LDGSTS): every element's load is in flight
 // at once instead of one load latency per loop trip. Gathered tiles move each
@@ -361,7 +422,7 @@ __device__ __forceinline__ void cp_async_wait_all() {
 }
 template <typename R, int WD>
 __device__ __forceinline__ void tile_in(R* dst, const R* src, const int32_t* srow, int64_t base, int n) {
-  for (int e = threadIdx.x; e < n * WD; e += kThreads) {
+  for (int e = threadIdx.x; e < n * WD; e += blockDim.x) {
     const int r = e / WD, c = e - r * WD;
     const int64_t row = srow ? int64_t(srow[r]) : base + r;
     cp_async_elem(dst + e, src + row * WD + c);
@@ -370,10 +431,10 @@ __device__ __forceinline__ void tile_in(R* dst, const R* src, const int32_t* sro
 template <typename R, int WD>
 __device__ __forceinline__ void tile_out(R* dst, const R* src, const int32_t* srow, int64_t base, int n) {
   if (srow == nullptr) {
-    for (int e = threadIdx.x; e < n * WD; e += kThreads) dst[base * WD + e] = src[e];
+    for (int e = threadIdx.x; e < n * WD; e += blockDim.x) dst[base * WD + e] = src[e];
     return;
   }
-  for (int e = threadIdx.x; e < n * WD; e += kThreads) {
+  for (int e = threadIdx.x; e < n * WD; e += blockDim.x) {
     const int r = e / WD, c = e - r * WD;
     dst[int64_t(srow[r]) * WD + c] = src[e];
   }
@@ -483,6 +544,54 @@ __device__ __forceinline__ void tile_compute(const PathArgs<R>& a, const int32_t
   __syncthreads();
 }
 
+// Paired tile (kThreads / 2 threads): thread t takes the tile's paths t and
+// t + kThreads / 2. When both exist, share a kind mask and the loop is the
+// common form, they run the paired loop (run_pair); otherwise each runs its
+// own per-path variant in turn. A path's bits are the same either way.
+template <int K, int OP>
+__device__ __forceinline__ void tile_compute_pair(const PathArgs<float>& a, const int32_t* srow,
+                                                  int64_t base, int n, unsigned char* slab) {
+  using Wk = W<K, OP>;
+  constexpr int NT = kThreads / 2;
+  const int ta = threadIdx.x, tb = threadIdx.x + NT;
+  const bool has_v = Wk::has_v && a.vT != nullptr;
+  const InSlab<float, K, OP> sl(slab);
+  Rec<float, K> ra, rb;
+  if (ta < n)
+    load_rec(ra, sl.b + ta * Wk::basis, sl.a + ta * Wk::anchor, sl.x0 + ta * 3, sl.x1 + ta * 3,
+             sl.T + ta * Wk::T, has_v ? sl.v + ta * Wk::T : nullptr);
+  if (tb < n)
+    load_rec(rb, sl.b + tb * Wk::basis, sl.a + tb * Wk::anchor, sl.x0 + tb * 3, sl.x1 + tb * 3,
+             sl.T + tb * Wk::T, has_v ? sl.v + tb * Wk::T : nullptr);
+  __syncthreads();
+  if (ta < n) {
+    const int64_t rowa = srow ? int64_t(srow[ta]) : base + ta;
+    const unsigned ma = rec_mask<float, K>(ra);
+    const bool two = tb < n;
+    const unsigned mb = two ? rec_mask<float, K>(rb) : ma;
+    if (a.mixed_warps != nullptr) {
+      // one warp covers 64 paths: count it twice (the host's fraction is per 32 paths)
+      const unsigned act = __activemask();
+      const unsigned key = (two && ma != mb) ? 0xFFFFFFFFu : ma;
+      if ((__match_any_sync(act, key) != act || key == 0xFFFFFFFFu) && (threadIdx.x & 31) == __ffs(act) - 1)
+        atomicAdd(a.mixed_warps, 2ull);
+    }
+    const bool loop_common = a.fp_iters == 1 && a.trace_len == nullptr && a.H_out == nullptr;
+    if (two && ma == mb && loop_common) {
+      const int64_t rowb = srow ? int64_t(srow[tb]) : base + tb;
+      run_pair_any_mask<K, OP>(ma, a, rowa, rowb, ra, rb, has_v, ta, tb, slab);
+    } else {
+      run_any_mask<float, K, OP>(ma, a, rowa, ra, has_v, ta, slab);
+      if (two) {
+        const int64_t rowb = srow ? int64_t(srow[tb]) : base + tb;
+        run_any_mask<float, K, OP>(mb, a, rowb, rb, has_v, tb, slab);
+      }
+    }
+  }
+  fence_async_smem();
+  __syncthreads();
+}
+
 // One thread: TMA bulk stores of a full aligned tile's output runs (committed
 // as one bulk group; the caller waits for the reads before reusing the slab).
 template <typename R, int K, int OP>
@@ -531,7 +640,7 @@ __device__ __forceinline__ void tile_store_coop(const PathArgs<R>& a, const int3
 // One tile per CTA: stage inputs (TMA bulk copies for full aligned contiguous
 // tiles, cp.async otherwise), compute in registers, stage the outputs and
 // write them back (TMA bulk stores when full and aligned).
-template <typename R, int K, unsigned MASK, int OP>
+template <typename R, int K, unsigned MASK, int OP, bool PAIR = false>
 __device__ __forceinline__ void process_tile(const PathArgs<R>& a, const int32_t* srow, int64_t base,
                                              int n, uint64_t* bar) {
   const int tid = threadIdx.x;
@@ -546,7 +655,10 @@ __device__ __forceinline__ void process_tile(const PathArgs<R>& a, const int32_t
     tile_load_async<R, K, OP>(a, srow, base, n, slab);
     __syncthreads();
   }
-  tile_compute<R, K, MASK, OP>(a, srow, base, n, slab);
+  if constexpr (PAIR)
+    tile_compute_pair<K, OP>(a, srow, base, n, slab);
+  else
+    tile_compute<R, K, MASK, OP>(a, srow, base, n, slab);
   if (full && tile_out_aligned<R, K, OP>(a, base)) {
     if (tid == 0) {
       tile_store_tma<R, K, OP>(a, base, slab);
@@ -618,8 +730,29 @@ struct LaunchMin {
                                    : FP_TILE_MIN_BLOCKS_K5);
 };
 
-template <typename R, int K, unsigned MASK, int OP>
-__global__ void __launch_bounds__(kThreads, (LaunchMin<R, K, MASK>::value))
+// Paired tile kernels (fp32, kThreads / 2 threads, two paths per thread;
+// fp_pair.cuh): CTAs per SM requested from ptxas. FP_PAIR_MIN_BLOCKS_K<k>
+// overrides.
+#ifndef FP_PAIR_MIN_BLOCKS_K1
+#define FP_PAIR_MIN_BLOCKS_K1 8
+#endif
+#ifndef FP_PAIR_MIN_BLOCKS_K2
+#define FP_PAIR_MIN_BLOCKS_K2 4
+#endif
+template <int K>
+struct PairMin {
+  static constexpr int value = K == 1 ? FP_PAIR_MIN_BLOCKS_K1 : K == 2 ? FP_PAIR_MIN_BLOCKS_K2 : 4;
+};
+
+template <typename R, int K, unsigned MASK, int OP, bool PAIR>
+struct KernelShape {
+  static constexpr int threads = PAIR ? kThreads / 2 : kThreads;
+  static constexpr int min_blocks = PAIR ? PairMin<K>::value : LaunchMin<R, K, MASK>::value;
+};
+
+template <typename R, int K, unsigned MASK, int OP, bool PAIR = false>
+__global__ void __launch_bounds__((KernelShape<R, K, MASK, OP, PAIR>::threads),
+                                  (KernelShape<R, K, MASK, OP, PAIR>::min_blocks))
     path_kernel(const __grid_constant__ PathArgs<R> a) {
   __shared__ __align__(8) uint64_t bar;
   __shared__ int32_t srow[kThreads];
@@ -628,23 +761,25 @@ __global__ void __launch_bounds__(kThreads, (LaunchMin<R, K, MASK>::value))
     const int64_t t0 = int64_t(blockIdx.x) * kThreads;
     if (t0 >= a.n_rows) return;
     const int n = int(a.n_rows - t0 < kThreads ? a.n_rows - t0 : int64_t(kThreads));
-    if (tid < n) srow[tid] = a.rows[t0 + tid];
+    for (int i = tid; i < n; i += blockDim.x) srow[i] = a.rows[t0 + i];
     __syncthreads();
-    process_tile<R, K, MASK, OP>(a, srow, 0, n, &bar);
+    process_tile<R, K, MASK, OP, PAIR>(a, srow, 0, n, &bar);
     return;
   }
   const int64_t base = a.row_begin + int64_t(blockIdx.x) * kThreads;
   if (base >= a.B) return;
   const int n = int(a.B - base < kThreads ? a.B - base : int64_t(kThreads));
-  process_tile<R, K, MASK, OP>(a, nullptr, base, n, &bar);
+  process_tile<R, K, MASK, OP, PAIR>(a, nullptr, base, n, &bar);
 }
 
 // Host-side launcher (defined per K in fp_inst.cu).
 template <typename R, int K, unsigned MASK, int OP>
 cudaError_t launch_path(const PathArgs<R>& a, cudaStream_t stream);
 
-template <typename R, int K, unsigned MASK, int OP>
+template <typename R, int K, unsigned MASK, int OP, bool PAIR = false>
 cudaError_t launch_path_impl(const PathArgs<R>& a, cudaStream_t stream) {
+  static_assert(!PAIR || (std::is_same<R, float>::value && MASK == kAnyMask && OP != OP_VJP),
+                "paired kernels: fp32 tile solves only");
   const int64_t rows = a.rows ? a.n_rows : a.B - a.row_begin;
   if (rows <= 0) return cudaSuccess;
   constexpr size_t smem = smem_bytes<R, K, OP>();
@@ -656,13 +791,14 @@ cudaError_t launch_path_impl(const PathArgs<R>& a, cudaStream_t stream) {
   if (e != cudaSuccess) return e;
   const uint64_t bit = 1ull << (dev & 63);
   if (!(configured.load(std::memory_order_acquire) & bit)) {
-    e = cudaFuncSetAttribute(path_kernel<R, K, MASK, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(smem));
+    e = cudaFuncSetAttribute(path_kernel<R, K, MASK, OP, PAIR>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     configured.fetch_or(bit, std::memory_order_acq_rel);
   }
   const int64_t blocks = (rows + kThreads - 1) / kThreads;
-  path_kernel<R, K, MASK, OP><<<dim3(unsigned(blocks)), dim3(kThreads), smem, stream>>>(a);
+  path_kernel<R, K, MASK, OP, PAIR>
+      <<<dim3(unsigned(blocks)), dim3(KernelShape<R, K, MASK, OP, PAIR>::threads), smem, stream>>>(a);
   return cudaGetLastError();
 }
 
