@@ -4,7 +4,7 @@
 // MAX_INTERACTIONS); the register-resident kernels stop at order 8. Here one
 // warp owns one path: the dense 2K formulation (edges carry their zero basis
 // column, geometry.py:86-90), the inverse Hessian and the per-path vectors in
-// shared memory (row stride m + 1, so a row per lane is bank-conflict free),
+// shared memory (16-byte row reads, a bank-conflict-free row stride),
 // lanes striding over interactions, segments and Hessian rows, reductions as
 // warp butterflies. The operations follow the reference's batched code in
 // order — embed / clamped segments / gradient (batching.py:83-126), the
@@ -42,41 +42,64 @@ __device__ __forceinline__ R warp_min(R v) {
   return v;
 }
 
-// Per-warp shared-memory layout (units of R).
+// Per-warp shared-memory layout (units of R). Every array starts on a
+// 16-byte boundary, so the BFGS loop reads H rows and the broadcast vectors
+// with 16-byte loads; the H row stride makes those row reads bank-conflict
+// free (a stride of 4 x odd words: the 8 lanes of each 128-byte phase hit
+// distinct 4-bank groups).
 struct WideLayout {
   int K, m, S, ld;
   int H, t, g, gn, p, st, y, hy, A, b, x, s, nc, nu, u, d, a2c, D, O, rhs, act, sol, dx, w, red;
   int total;
-  __host__ __device__ explicit WideLayout(int k) : K(k), m(2 * k), S(k + 1), ld(2 * k + 1) {
+  __host__ __device__ static int row_stride(int m, int esize) {
+    int ld = m;
+    if (esize == 4)
+      while (ld % 8 != 4) ++ld;  // ld words
+    else
+      while (ld % 4 != 2) ++ld;  // 2 ld words
+    return ld;
+  }
+  __host__ __device__ WideLayout(int k, int esize)
+      : K(k), m(2 * k), S(k + 1), ld(row_stride(2 * k, esize)) {
     int o = 0;
-    H = o; o += m * ld;
-    t = o; o += m;
-    g = o; o += m;
-    gn = o; o += m;
-    p = o; o += m;
-    st = o; o += m;
-    y = o; o += m;
-    hy = o; o += m;
-    A = o; o += 6 * K;
-    b = o; o += 3 * K;
-    x = o; o += 3 * (K + 2);
-    s = o; o += 3 * S;
-    nc = o; o += S;
-    nu = o; o += S;
-    u = o; o += 3 * S;
-    d = o; o += 3 * S;
-    a2c = o; o += 2 * S;
-    D = o; o += 3 * K;
-    O = o; o += 4 * K;
-    rhs = o; o += 2 * K;
-    act = o; o += 2 * K;
-    sol = o; o += 2 * K;
-    dx = o; o += 3 * K;
-    w = o; o += 3 * S;
-    red = o; o += 8;
-    total = (o + 1) & ~1;  // keep every warp's block 16-byte aligned for doubles
+    auto take = [&o](int n) {
+      const int r = o;
+      o += (n + 3) & ~3;  // 4 elements: 16 bytes (fp32), 32 bytes (fp64)
+      return r;
+    };
+    H = take(m * ld);
+    t = take(m);
+    g = take(m);
+    gn = take(m);
+    p = take(m);
+    st = take(m);
+    y = take(m);
+    hy = take(m);
+    A = take(6 * K);
+    b = take(3 * K);
+    x = take(3 * (K + 2));
+    s = take(3 * S);
+    nc = take(S);
+    nu = take(S);
+    u = take(3 * S);
+    d = take(3 * S);
+    a2c = take(2 * S);
+    D = take(3 * K);
+    O = take(4 * K);
+    rhs = take(2 * K);
+    act = take(2 * K);
+    sol = take(2 * K);
+    dx = take(3 * K);
+    w = take(3 * S);
+    red = take(8);
+    total = o;
   }
 };
+
+// 16-byte vectors of R (four floats, two doubles).
+template <typename R> struct Vec16;
+template <> struct Vec16<float> { using T = float4; static constexpr int W = 4; };
+template <> struct Vec16<double> { using T = double2; static constexpr int W = 2; };
 
 template <typename R>
 struct WideCtx {
@@ -145,17 +168,111 @@ __device__ R wide_dot(const WideCtx<R>& c, const R* a, const R* b) {
   return warp_sum(acc);
 }
 
-// out = H v (rows across lanes).
-template <typename R>
-__device__ void wide_matvec(const WideCtx<R>& c, const R* v, R* out, R sign) {
+// out = H v (rows across lanes; each row and v read as 16-byte vectors, the
+// products accumulated in column order). A lane's rows (j, j + 32, ...) run
+// their chains side by side: independent FMA chains hide each other's latency.
+template <typename R, int NR>
+__device__ __forceinline__ void wide_matvec_rows(const WideCtx<R>& c, const R* v, R* out, R sign) {
+  using V = typename Vec16<R>::T;
+  constexpr int W = Vec16<R>::W;
   const WideLayout& L = c.L;
-  for (int j = c.lane; j < L.m; j += 32) {
-    const R* h = c.sm + L.H + j * L.ld;
-    R acc = R(0);
-    for (int q = 0; q < L.m; ++q) acc = fma(h[q], v[q], acc);
-    out[j] = sign * acc;
+  const R* h[NR];
+  R acc[NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const int j = c.lane + 32 * r;
+    h[r] = c.sm + L.H + (j < L.m ? j : 0) * L.ld;  // past the last row: row 0, result dropped
+    acc[r] = R(0);
   }
+  int q = 0;
+  for (; q + W <= L.m; q += W) {
+    const V vv = *reinterpret_cast<const V*>(v + q);
+    const R* ve = reinterpret_cast<const R*>(&vv);
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const V hv = *reinterpret_cast<const V*>(h[r] + q);
+      const R* he = reinterpret_cast<const R*>(&hv);
+#pragma unroll
+      for (int e = 0; e < W; ++e) acc[r] = fma(he[e], ve[e], acc[r]);
+    }
+  }
+  for (; q < L.m; ++q)
+#pragma unroll
+    for (int r = 0; r < NR; ++r) acc[r] = fma(h[r][q], v[q], acc[r]);
+#pragma unroll
+  for (int r = 0; r < NR; ++r)
+    if (c.lane + 32 * r < L.m) out[c.lane + 32 * r] = sign * acc[r];
+}
+
+// NRMAX: the most rows a lane owns in this kernel instantiation (m <= 32 NRMAX).
+template <typename R, int NRMAX>
+__device__ void wide_matvec(const WideCtx<R>& c, const R* v, R* out, R sign) {
+  const int nr = (c.L.m + 31) / 32;  // rows per lane, warp-uniform (no divergence)
+  if (nr == 1) wide_matvec_rows<R, 1>(c, v, out, sign);
+  if constexpr (NRMAX >= 2) if (nr == 2) wide_matvec_rows<R, 2>(c, v, out, sign);
+  if constexpr (NRMAX >= 3) if (nr == 3) wide_matvec_rows<R, 3>(c, v, out, sign);
+  if constexpr (NRMAX >= 4) if (nr == 4) wide_matvec_rows<R, 4>(c, v, out, sign);
   __syncwarp();
+}
+
+// The BFGS update of the rows of this lane, the reference's expression per
+// entry (solver.py:186-195), rows side by side.
+template <typename R, int NR>
+__device__ __forceinline__ void wide_update_rows(const WideCtx<R>& c, const R* stp, const R* hy, R rho,
+                                                 R coef) {
+  using V = typename Vec16<R>::T;
+  constexpr int W = Vec16<R>::W;
+  const WideLayout& L = c.L;
+  R* h[NR];
+  R sj[NR], hj[NR];
+  bool live[NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const int j0 = c.lane + 32 * r;
+    live[r] = j0 < L.m;
+    const int j = live[r] ? j0 : 0;  // past the last row: row 0, computed, never stored
+    h[r] = c.sm + L.H + j * L.ld;
+    sj[r] = stp[j];
+    hj[r] = hy[j];
+  }
+  int q = 0;
+  for (; q + W <= L.m; q += W) {
+    const V sv = *reinterpret_cast<const V*>(stp + q);
+    const V yv = *reinterpret_cast<const V*>(hy + q);
+    const R* se = reinterpret_cast<const R*>(&sv);
+    const R* ye = reinterpret_cast<const R*>(&yv);
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      V hv = *reinterpret_cast<const V*>(h[r] + q);
+      R* he = reinterpret_cast<R*>(&hv);
+#pragma unroll
+      for (int e = 0; e < W; ++e)
+        he[e] = (he[e] - rho * (sj[r] * ye[e] + se[e] * hj[r])) + coef * (sj[r] * se[e]);
+      if (live[r]) *reinterpret_cast<V*>(h[r] + q) = hv;
+    }
+  }
+  for (; q < L.m; ++q)
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const R v = (h[r][q] - rho * (sj[r] * hy[q] + stp[q] * hj[r])) + coef * (sj[r] * stp[q]);
+      if (live[r]) h[r][q] = v;
+    }
+}
+
+template <typename R, int NRMAX>
+__device__ void wide_update(const WideCtx<R>& c, const R* stp, const R* hy, R rho, R coef) {
+  const int nr = (c.L.m + 31) / 32;
+  if (nr == 1) wide_update_rows<R, 1>(c, stp, hy, rho, coef);
+  if constexpr (NRMAX >= 2) if (nr == 2) wide_update_rows<R, 2>(c, stp, hy, rho, coef);
+  if constexpr (NRMAX >= 3) if (nr == 3) wide_update_rows<R, 3>(c, stp, hy, rho, coef);
+  if constexpr (NRMAX >= 4) if (nr == 4) wide_update_rows<R, 4>(c, stp, hy, rho, coef);
+}
+
+template <typename R>
+__device__ __forceinline__ R warp_absmax(R v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = absmax_nan(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
 }
 
 // Fixed-point step size along p (solver.py:84-112); sets `zero`.
@@ -444,13 +561,27 @@ __device__ uint8_t wide_vjp(const WideCtx<R>& c, const PathArgs<R>& a, int64_t r
   return st;
 }
 
-template <typename R, int OP>
-__global__ void __launch_bounds__(kWideThreads) wide_kernel(const __grid_constant__ PathArgs<R> a, int K,
+// One instantiation per bound on the rows a lane owns (NRMAX = 1: K <= 16,
+// 2: K <= 32, 4: K <= 64), so short orders do not pay the registers of the
+// four-row loops. CTAs per SM requested from ptxas: FP_WIDE_MIN_BLOCKS_R<n>
+// (A/B builds; K = 33..64 is shared-memory bound at one CTA per SM).
+#ifndef FP_WIDE_MIN_BLOCKS_R1
+#define FP_WIDE_MIN_BLOCKS_R1 6  // 80 registers; measured: K=16 fp32 3.97 -> 2.90 ms vs uncapped (153)
+#endif
+#ifndef FP_WIDE_MIN_BLOCKS_R2
+#define FP_WIDE_MIN_BLOCKS_R2 1
+#endif
+template <int NRMAX>
+struct WideMin {
+  static constexpr int value = NRMAX == 1 ? FP_WIDE_MIN_BLOCKS_R1 : NRMAX == 2 ? FP_WIDE_MIN_BLOCKS_R2 : 1;
+};
+template <typename R, int OP, int NRMAX>
+__global__ void __launch_bounds__(kWideThreads, WideMin<NRMAX>::value) wide_kernel(const __grid_constant__ PathArgs<R> a, int K,
                                                             int wpb) {
   extern __shared__ __align__(16) unsigned char wide_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp >= wpb) return;
-  const WideLayout L(K);
+  const WideLayout L(K, int(sizeof(R)));
   const int64_t row = a.row_begin + int64_t(blockIdx.x) * wpb + warp;
   if (row >= a.B) return;  // whole warp leaves together: only warp-level sync below
   R* sm = reinterpret_cast<R*>(wide_smem) + size_t(warp) * L.total;
@@ -483,6 +614,7 @@ __global__ void __launch_bounds__(kWideThreads) wide_kernel(const __grid_constan
     R* H = sm + L.H;
     for (int j = lane; j < m; j += 32)
       for (int q = 0; q < m; ++q) H[j * L.ld + q] = j == q ? R(1) : R(0);
+    R hbound = R(1);  // >= max |H_ij| (the update's overflow pre-check)
     R* p = sm + L.p;
     R* stp = sm + L.st;
     R* gn = sm + L.gn;
@@ -490,7 +622,7 @@ __global__ void __launch_bounds__(kWideThreads) wide_kernel(const __grid_constan
     R* hy = sm + L.hy;
     __syncwarp();
     for (int it = 0; it < a.iterations; ++it) {
-      wide_matvec(c, g, p, R(-1));  // p = -H g
+      wide_matvec<R, NRMAX>(c, g, p, R(-1));  // p = -H g
       bool zero;
       const R alpha = wide_step_size(c, p, a.fp_iters, zero);
       if (zero) st |= FP_STATUS_ZERO_DIRECTION;
@@ -509,24 +641,47 @@ __global__ void __launch_bounds__(kWideThreads) wide_kernel(const __grid_constan
       if (!(sy > (R(1e-12) * sn) * yn)) fate |= FP_FATE_CURVATURE_SKIP;
       if (sy > (R(1e-12) * sn) * yn) {
         const R rho = R(1) / sy;
-        wide_matvec(c, y, hy, R(1));
+        wide_matvec<R, NRMAX>(c, y, hy, R(1));
         const R yHy = wide_dot(c, y, hy);
         const R coef = rho * rho * yHy + rho;
-        bool fin = true;
+        // The reference skips the update when any entry of H' is not finite
+        // (solver.py:196-199). With ms = max|s|, mh = max|Hy| and bound >=
+        // max|H|, every intermediate of an entry is at most 2 ms mh, ms^2,
+        // 2 |rho| ms mh, |coef| ms^2 or bound + 2 |rho| ms mh + |coef| ms^2;
+        // below Num<R>::suspect() (340x / 1800x under the largest finite
+        // value) none can overflow, so the entry-by-entry check runs only
+        // above it (or on a NaN, which the NaN-propagating maxima carry).
+        // Same verdicts as checking every entry.
+        R ms = R(0), mh = R(0);
         for (int j = lane; j < m; j += 32) {
-          const R* h = H + j * L.ld;
-          for (int q = 0; q < m; ++q) {
-            const R v = (h[q] - rho * (stp[j] * hy[q] + stp[q] * hy[j])) + coef * (stp[j] * stp[q]);
-            fin = fin && finite(v);
-          }
+          ms = absmax_nan(ms, stp[j]);
+          mh = absmax_nan(mh, hy[j]);
         }
-        if (!__all_sync(0xffffffffu, fin)) fate |= FP_FATE_NONFINITE_SKIP;
-        if (__all_sync(0xffffffffu, fin)) {
+        ms = warp_absmax(ms);
+        mh = warp_absmax(mh);
+        const R am = ms * mh, ss = ms * ms;
+        const R r2a = R(2) * fabs(rho) * am, cs = fabs(coef) * ss;
+        const R nb = (hbound + r2a) + cs;
+        const R big = absmax_nan(absmax_nan(R(2) * am, ss), absmax_nan(absmax_nan(r2a, cs), nb));
+        bool fin = true;
+        R mx = R(0);
+        const bool checked = !(big < Num<R>::suspect());
+        if (checked) {
           for (int j = lane; j < m; j += 32) {
-            R* h = H + j * L.ld;
-            for (int q = 0; q < m; ++q)
-              h[q] = (h[q] - rho * (stp[j] * hy[q] + stp[q] * hy[j])) + coef * (stp[j] * stp[q]);
+            const R* h = H + j * L.ld;
+            for (int q = 0; q < m; ++q) {
+              const R v = (h[q] - rho * (stp[j] * hy[q] + stp[q] * hy[j])) + coef * (stp[j] * stp[q]);
+              fin = fin && finite(v);
+              mx = fabs(v) > mx ? fabs(v) : mx;
+            }
           }
+          fin = __all_sync(0xffffffffu, fin);
+          mx = warp_absmax(mx);
+        }
+        if (!fin) fate |= FP_FATE_NONFINITE_SKIP;
+        if (fin) {
+          wide_update<R, NRMAX>(c, stp, hy, rho, coef);
+          hbound = checked ? mx * R(1.0009765625) : nb;
         }
         __syncwarp();
       }
@@ -573,7 +728,11 @@ __global__ void __launch_bounds__(kWideThreads) wide_kernel(const __grid_constan
 
 }  // namespace
 
-size_t wide_smem_per_path(int K, size_t elem) { return size_t(WideLayout(K).total) * elem; }
+size_t wide_smem_per_path(int K, size_t elem) { return size_t(WideLayout(K, int(elem)).total) * elem; }
+
+template <typename R, int NRMAX>
+cudaError_t launch_wide(int op, const PathArgs<R>& a, int K, int wpb, int64_t blocks, int threads,
+                        size_t smem, cudaStream_t s);
 
 template <typename R>
 cudaError_t dispatch_wide(int K, const PathArgs<R>& a, int op, cudaStream_t s) {
@@ -590,22 +749,34 @@ cudaError_t dispatch_wide(int K, const PathArgs<R>& a, int op, cudaStream_t s) {
   const size_t smem = per * size_t(wpb);
   const int64_t blocks = (rows + wpb - 1) / wpb;
   const int threads = 32 * wpb;
+  const int nrmax = (2 * K + 31) / 32;
+  switch (nrmax) {
+    case 1: return launch_wide<R, 1>(op, a, K, wpb, blocks, threads, smem, s);
+    case 2: return launch_wide<R, 2>(op, a, K, wpb, blocks, threads, smem, s);
+    default: return launch_wide<R, 4>(op, a, K, wpb, blocks, threads, smem, s);
+  }
+}
+
+template <typename R, int NRMAX>
+cudaError_t launch_wide(int op, const PathArgs<R>& a, int K, int wpb, int64_t blocks, int threads,
+                        size_t smem, cudaStream_t s) {
   cudaError_t e;
   switch (op) {
     case OP_SOLVE:
-      e = cudaFuncSetAttribute(wide_kernel<R, OP_SOLVE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      if (e == cudaSuccess)
-        wide_kernel<R, OP_SOLVE><<<unsigned(blocks), threads, smem, s>>>(a, K, wpb);
+      e = cudaFuncSetAttribute(wide_kernel<R, OP_SOLVE, NRMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(smem));
+      if (e == cudaSuccess) wide_kernel<R, OP_SOLVE, NRMAX><<<unsigned(blocks), threads, smem, s>>>(a, K, wpb);
       break;
     case OP_SOLVE_VJP:
-      e = cudaFuncSetAttribute(wide_kernel<R, OP_SOLVE_VJP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(smem));
+      e = cudaFuncSetAttribute(wide_kernel<R, OP_SOLVE_VJP, NRMAX>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       if (e == cudaSuccess)
-        wide_kernel<R, OP_SOLVE_VJP><<<unsigned(blocks), threads, smem, s>>>(a, K, wpb);
+        wide_kernel<R, OP_SOLVE_VJP, NRMAX><<<unsigned(blocks), threads, smem, s>>>(a, K, wpb);
       break;
     case OP_VJP:
-      e = cudaFuncSetAttribute(wide_kernel<R, OP_VJP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      if (e == cudaSuccess) wide_kernel<R, OP_VJP><<<unsigned(blocks), threads, smem, s>>>(a, K, wpb);
+      e = cudaFuncSetAttribute(wide_kernel<R, OP_VJP, NRMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(smem));
+      if (e == cudaSuccess) wide_kernel<R, OP_VJP, NRMAX><<<unsigned(blocks), threads, smem, s>>>(a, K, wpb);
       break;
     default:
       return cudaErrorInvalidValue;
