@@ -678,6 +678,7 @@ __global__ void __launch_bounds__(kWideThreads, WideMin<NRMAX>::value) wide_kern
           fin = __all_sync(0xffffffffu, fin);
           mx = warp_absmax(mx);
         }
+        if (checked) fate |= FP_FATE_ENTRY_CHECK;
         if (!fin) fate |= FP_FATE_NONFINITE_SKIP;
         if (fin) {
           wide_update<R, NRMAX>(c, stp, hy, rho, coef);

@@ -181,6 +181,39 @@ def test_huge_inverse_hessians_entry_check_and_overflow_skips():
     assert agree_n >= (floor - 0.02) * agree_d
 
 
+def test_long_paths_overflow_check_and_skips():
+    """The long-path solver (orders 9..64, csrc/fp_wide.cu) in the same
+    huge-H regime: its update runs the all-entries finite check only when a
+    magnitude bound cannot exclude an overflow (FP_FATE_ENTRY_CHECK) and then
+    skips exactly the updates whose H' has a non-finite entry. Decisive fates
+    agree with the oracle at least as often as the reference with itself
+    (less 2 points); T stays finite; H stays finite where the oracle's does."""
+    checked = skips_dev = skips_ref = 0
+    agree_n = agree_d = 0
+    floors = []
+    for K, orders in ((9, ["RDRRDRDDR", "RRRRRRRRR"]), (12, ["RRDRRDRRDRRD"])):
+        for F, S in ((1e-3, 1e17), (1e-4, 1e16)):
+            b = datagen.gen_batch(700 + K, orders, 96 // len(orders))
+            b.basis *= np.float32(F)
+            res, ref = _run(b, 40, np.float32, scale=S)
+            agree, f = _agreement(res, ref)
+            dec = _decisive(ref)
+            agree_n += int(agree[dec].sum())
+            agree_d += int(dec.sum())
+            floors.append(_self_agreement(b, 40, np.float32, scale=S))
+            checked += int(((f & _lib.FATE_ENTRY_CHECK) != 0).sum())
+            skips_dev += int(((f & _lib.FATE_NONFINITE_SKIP) != 0).sum())
+            skips_ref += int(((ref["trace_fate"] & _lib.FATE_NONFINITE_SKIP) != 0).sum())
+            assert np.isfinite(res.T.cpu().numpy()).all()
+            H_fin_ref = np.isfinite(ref["H"]).all(axis=(1, 2))
+            assert np.isfinite(res.H.cpu().numpy()).all(axis=(1, 2))[H_fin_ref].all()
+    floor = float(np.mean(floors))
+    print(f"long paths: entry checks {checked}, non-finite skips device {skips_dev} oracle {skips_ref}, "
+          f"decisive agreement {agree_n / max(agree_d, 1):.4f} of {agree_d} (self-agreement {floor:.4f})")
+    assert checked >= 1 and skips_dev >= 1 and skips_ref >= 1
+    assert agree_n >= (floor - 0.02) * agree_d
+
+
 @pytest.mark.parametrize("prec", ["f32", "f64"])
 def test_nonfinite_inputs_stay_in_their_rows(prec):
     """NaN / Inf in the basis, anchor, start or end of some rows: those rows
