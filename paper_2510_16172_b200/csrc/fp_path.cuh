@@ -624,6 +624,12 @@ __device__ __forceinline__ bool stationary(const V2<R> (&g)[Packed<NA>::NP], R l
   return Num<R>::sqrt_(norm2_seq<R, NA>(g)) < R(1e-5) * (R(1) + len);
 }
 
+#ifndef FP_SKIP_LAST_MIN_K
+#define FP_SKIP_LAST_MIN_K 2
+#endif
+#ifndef FP_SKIP_LAST_MAX_K
+#define FP_SKIP_LAST_MAX_K 4
+#endif
 #ifndef FP_UNROLL_MAX_K
 #define FP_UNROLL_MAX_K 1
 #endif
@@ -638,11 +644,21 @@ __device__ __forceinline__ void bfgs_iterations(const Geo<R, K>& G, PathState<R,
                                                 V2<R> (&p)[Packed<Lay<K, MASK>::NA>::NP], uint8_t& st,
                                                 int iterations, int fp_iters_rt, R* trace_len,
                                                 R* trace_gnorm, uint8_t* trace_fate, int64_t trace_ld,
-                                                int64_t row) {
+                                                int64_t row, bool keep_last_update = true) {
   using L = Lay<K, MASK>;
   constexpr int NA = L::NA;
   constexpr int NP = Packed<NA>::NP;
   const int fp_iters = GENERAL ? fp_iters_rt : 1;
+  // The last iteration's curvature test, inverse-Hessian update and next
+  // direction feed nothing the caller reads unless it returns H (or traces
+  // the update fates): without them the last iteration ends at its new
+  // gradient. Every output is bitwise the same. Measured (profiles/
+  // r02t_ab_last.txt): K=3 fused 1.043 -> 1.021 ms, K=4 1.452 -> 1.443, K=2
+  // 0.718 -> 0.716, config-3 walls 71.2 -> 69.5 ms; K=1 (loop unrolled by
+  // two) 0.411 -> 0.417 and K=5 (out-of-line variants) 2.006 -> 2.026, so
+  // orders 1 and 5+ keep the full last iteration.
+  constexpr bool kMaySkipLast = !GENERAL && K >= FP_SKIP_LAST_MIN_K && K <= FP_SKIP_LAST_MAX_K;
+  const int last = (kMaySkipLast && !keep_last_update) ? iterations - 1 : -1;
   // Short loop bodies (order 1) run two iterations per trip: -1.2% at K=1
   // (tools/ab_libs.sh; at K=3 unrolling measured slower, instruction cache).
   constexpr int kUnroll = (K <= kUnrollMaxOrder && !GENERAL) ? 2 : 1;
@@ -660,6 +676,11 @@ __device__ __forceinline__ void bfgs_iterations(const Geo<R, K>& G, PathState<R,
     }
     V2<R> gn[NP];
     P.template eval<true>(G, gn);
+    if (it == last) {
+#pragma unroll
+      for (int m = 0; m < NP; ++m) P.g[m] = gn[m];
+      break;
+    }
     V2<R> y[NP];
 #pragma unroll
     for (int m = 0; m < NP; ++m) y[m] = sub2p((NA & 1) && m == NP - 1, gn[m], P.g[m]);
@@ -722,7 +743,8 @@ __device__ __forceinline__ uint8_t bfgs_solve(const Geo<R, K>& G, PathState<R, K
   for (int m = 0; m < NP; ++m) p[m] = neg2(P.g[m]);  // H = I
 #ifndef FP_NO_LOOP_SPECIALISATION
   if (fp_iters == 1 && trace_len == nullptr)
-    bfgs_iterations<R, K, MASK, false>(G, P, H, p, st, iterations, 1, nullptr, nullptr, nullptr, 0, 0);
+    bfgs_iterations<R, K, MASK, false>(G, P, H, p, st, iterations, 1, nullptr, nullptr, nullptr, 0, 0,
+                                       H_out != nullptr);
   else
 #endif
     bfgs_iterations<R, K, MASK, true>(G, P, H, p, st, iterations, fp_iters, trace_len, trace_gnorm,

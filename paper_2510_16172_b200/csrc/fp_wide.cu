@@ -615,6 +615,7 @@ __global__ void __launch_bounds__(kWideThreads, WideMin<NRMAX>::value) wide_kern
     for (int j = lane; j < m; j += 32)
       for (int q = 0; q < m; ++q) H[j * L.ld + q] = j == q ? R(1) : R(0);
     R hbound = R(1);  // >= max |H_ij| (the update's overflow pre-check)
+    const bool last_dead = a.H_out == nullptr && a.trace_len == nullptr;
     R* p = sm + L.p;
     R* stp = sm + L.st;
     R* gn = sm + L.gn;
@@ -633,6 +634,12 @@ __global__ void __launch_bounds__(kWideThreads, WideMin<NRMAX>::value) wide_kern
       }
       __syncwarp();
       wide_eval(c, t, gn);
+      if (last_dead && it == a.iterations - 1) {
+        // the last update and its curvature test feed nothing read afterwards
+        for (int j = lane; j < m; j += 32) g[j] = gn[j];
+        __syncwarp();
+        break;
+      }
       for (int j = lane; j < m; j += 32) y[j] = gn[j] - g[j];
       __syncwarp();
       const R sy = wide_dot(c, stp, y);
