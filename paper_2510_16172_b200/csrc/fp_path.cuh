@@ -624,11 +624,11 @@ __device__ __forceinline__ bool stationary(const V2<R> (&g)[Packed<NA>::NP], R l
   return Num<R>::sqrt_(norm2_seq<R, NA>(g)) < R(1e-5) * (R(1) + len);
 }
 
-#ifndef FP_SKIP_LAST_MIN_K
-#define FP_SKIP_LAST_MIN_K 2
+#ifndef FP_LAST_BREAK_ORDERS
+#define FP_LAST_BREAK_ORDERS 0x08u  // order 3
 #endif
-#ifndef FP_SKIP_LAST_MAX_K
-#define FP_SKIP_LAST_MAX_K 4
+#ifndef FP_LAST_PEEL_ORDERS
+#define FP_LAST_PEEL_ORDERS 0x16u  // orders 1, 2, 4
 #endif
 #ifndef FP_UNROLL_MAX_K
 #define FP_UNROLL_MAX_K 1
@@ -652,31 +652,41 @@ __device__ __forceinline__ void bfgs_iterations(const Geo<R, K>& G, PathState<R,
   // The last iteration's curvature test, inverse-Hessian update and next
   // direction feed nothing the caller reads unless it returns H (or traces
   // the update fates): without them the last iteration ends at its new
-  // gradient. Every output is bitwise the same. Measured (profiles/
-  // r02t_ab_last.txt): K=3 fused 1.043 -> 1.021 ms, K=4 1.452 -> 1.443, K=2
-  // 0.718 -> 0.716, config-3 walls 71.2 -> 69.5 ms; K=1 (loop unrolled by
-  // two) 0.411 -> 0.417 and K=5 (out-of-line variants) 2.006 -> 2.026, so
-  // orders 1 and 5+ keep the full last iteration.
-  constexpr bool kMaySkipLast = !GENERAL && K >= FP_SKIP_LAST_MIN_K && K <= FP_SKIP_LAST_MAX_K;
-  const int last = (kMaySkipLast && !keep_last_update) ? iterations - 1 : -1;
-  // Short loop bodies (order 1) run two iterations per trip: -1.2% at K=1
-  // (tools/ab_libs.sh; at K=3 unrolling measured slower, instruction cache).
-  constexpr int kUnroll = (K <= kUnrollMaxOrder && !GENERAL) ? 2 : 1;
-#pragma unroll(kUnroll)
-  for (int it = 0; it < iterations; ++it) {
-    bool zero;
+  // gradient. Every output is bitwise the same. Two forms, per order
+  // (FP_LAST_BREAK_ORDERS / FP_LAST_PEEL_ORDERS, bit K): leave the loop after
+  // the last evaluation, or peel the last iteration out of the loop.
+  // Measured (profiles/r02t_ab_last.txt, r02v_ab_peel.txt; fused step):
+  // break K=3 1.043 -> 1.021 ms (peel 1.029), config-3 walls 71.2 -> 69.5
+  // ms; peel K=1 0.411 -> 0.4025 (break 0.417: the loop is unrolled by two),
+  // K=2 0.7155 -> 0.704 (break 0.712), K=4 1.443 -> 1.4415 with the forward
+  // 1.281 -> 1.263; K=5 (out-of-line variants) keeps the full iteration
+  // (break 2.026, peel 2.044 vs 2.004).
+  constexpr bool kBreakLast = !GENERAL && ((FP_LAST_BREAK_ORDERS >> K) & 1);
+  constexpr bool kPeelLast = !GENERAL && !kBreakLast && ((FP_LAST_PEEL_ORDERS >> K) & 1);
+  const bool short_last = (kBreakLast || kPeelLast) && !keep_last_update && iterations > 0;
+  const int last = (kBreakLast && short_last) ? iterations - 1 : -1;
+  const int n_loop = (kPeelLast && short_last) ? iterations - 1 : iterations;
+  // one step along p and the evaluation at the new t
+  auto advance = [&](V2<R> (&sg)[NP], V2<R> (&gn)[NP], bool& zero) {
     const R alpha = P.step_size(G, p, fp_iters, zero);
     if (zero) st |= FP_STATUS_ZERO_DIRECTION;
-    V2<R> sg[NP];
 #pragma unroll
     for (int m = 0; m < NP; ++m) {
       const bool lo = (NA & 1) && m == NP - 1;  // padding high lane
       sg[m] = mulzp(lo, bc2(alpha), p[m], G.nz);
       P.t[m] = add2p(lo, P.t[m], sg[m]);
     }
-    V2<R> gn[NP];
     P.template eval<true>(G, gn);
-    if (it == last) {
+  };
+  // Short loop bodies (order 1) run two iterations per trip: -1.2% at K=1
+  // (tools/ab_libs.sh; at K=3 unrolling measured slower, instruction cache).
+  constexpr int kUnroll = (K <= kUnrollMaxOrder && !GENERAL) ? 2 : 1;
+#pragma unroll(kUnroll)
+  for (int it = 0; it < n_loop; ++it) {
+    bool zero;
+    V2<R> sg[NP], gn[NP];
+    advance(sg, gn, zero);
+    if (kBreakLast && it == last) {
 #pragma unroll
       for (int m = 0; m < NP; ++m) P.g[m] = gn[m];
       break;
@@ -718,6 +728,15 @@ __device__ __forceinline__ void bfgs_iterations(const Geo<R, K>& G, PathState<R,
       trace_gnorm[int64_t(it) * trace_ld + row] = Num<R>::sqrt_(norm2_seq<R, NA>(P.g));
       if (trace_fate != nullptr)
         trace_fate[int64_t(it) * trace_ld + row] = fate | (zero ? FP_FATE_ZERO_DIRECTION : 0);
+    }
+  }
+  if constexpr (kPeelLast) {
+    if (n_loop < iterations) {
+      bool zero;
+      V2<R> sg[NP], gn[NP];
+      advance(sg, gn, zero);
+#pragma unroll
+      for (int m = 0; m < NP; ++m) P.g[m] = gn[m];
     }
   }
 }
