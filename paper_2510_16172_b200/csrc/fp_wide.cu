@@ -2,7 +2,8 @@
 //
 // The reference accepts up to 64 interactions per path (geometry.py:23,
 // MAX_INTERACTIONS); the register-resident kernels stop at order 8. Here one
-// warp owns one path: the dense 2K formulation (edges carry their zero basis
+// warp owns one path (two paths per warp, 16 lanes each, up to order 15 in
+// fp32 / 11 in fp64): the dense 2K formulation (edges carry their zero basis
 // column, geometry.py:86-90), the inverse Hessian and the per-path vectors in
 // shared memory (16-byte row reads, a bank-conflict-free row stride),
 // lanes striding over interactions, segments and Hessian rows, reductions as
@@ -26,17 +27,17 @@ namespace {
 constexpr int kWideMaxOrder = 64;
 constexpr int kWideThreads = 128;  // 4 paths per CTA when shared memory allows
 
+// Reductions over the lanes of one path: a whole warp (lp = 32) or an aligned
+// half (lp = 16, two paths per warp; gm masks the half).
 template <typename R>
-__device__ __forceinline__ R warp_sum(R v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+__device__ __forceinline__ R warp_sum(R v, int lp, unsigned gm) {
+  for (int o = lp >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(gm, v, o);
   return v;
 }
 template <typename R>
-__device__ __forceinline__ R warp_min(R v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const R w = __shfl_xor_sync(0xffffffffu, v, o);
+__device__ __forceinline__ R warp_min(R v, int lp, unsigned gm) {
+  for (int o = lp >> 1; o > 0; o >>= 1) {
+    const R w = __shfl_xor_sync(gm, v, o);
     v = w < v ? w : v;
   }
   return v;
@@ -105,7 +106,9 @@ template <typename R>
 struct WideCtx {
   WideLayout L;
   R* sm;
-  int lane;
+  int lane;     // lane within the path's lanes
+  int lp;       // lanes per path (32, or 16: two paths per warp)
+  unsigned gm;  // mask of the path's lanes
   R eps;
   __device__ R* at(int off) const { return sm + off; }
   __device__ R Aij(int i, int r, int c) const { return sm[L.A + 6 * i + 2 * r + c]; }
@@ -117,7 +120,7 @@ template <typename R>
 __device__ void wide_eval(const WideCtx<R>& c, const R* t, R* gout) {
   const WideLayout& L = c.L;
   R* sm = c.sm;
-  for (int q = c.lane; q < L.K + 2; q += 32) {
+  for (int q = c.lane; q < L.K + 2; q += c.lp) {
     R* X = sm + L.x + 3 * q;
     if (q == 0 || q == L.K + 1) continue;  // endpoints stored at load
     const int i = q - 1;
@@ -125,8 +128,8 @@ __device__ void wide_eval(const WideCtx<R>& c, const R* t, R* gout) {
     for (int r = 0; r < 3; ++r)
       X[r] = (c.Aij(i, r, 0) * t[2 * i] + c.Aij(i, r, 1) * t[2 * i + 1]) + sm[L.b + 3 * i + r];
   }
-  __syncwarp();
-  for (int k = c.lane; k < L.S; k += 32) {
+  __syncwarp(c.gm);
+  for (int k = c.lane; k < L.S; k += c.lp) {
     const R* lo = sm + L.x + 3 * k;
     const R* hi = lo + 3;
     R s[3];
@@ -142,8 +145,8 @@ __device__ void wide_eval(const WideCtx<R>& c, const R* t, R* gout) {
       sm[L.u + 3 * k + r] = Num<R>::div(s[r], cl);
     }
   }
-  __syncwarp();
-  for (int i = c.lane; i < L.K; i += 32) {
+  __syncwarp(c.gm);
+  for (int i = c.lane; i < L.K; i += c.lp) {
     R q[3];
 #pragma unroll
     for (int r = 0; r < 3; ++r) q[r] = sm[L.u + 3 * i + r] - sm[L.u + 3 * (i + 1) + r];
@@ -151,25 +154,25 @@ __device__ void wide_eval(const WideCtx<R>& c, const R* t, R* gout) {
     for (int cc = 0; cc < 2; ++cc)
       gout[2 * i + cc] = (c.Aij(i, 0, cc) * q[0] + c.Aij(i, 1, cc) * q[1]) + c.Aij(i, 2, cc) * q[2];
   }
-  __syncwarp();
+  __syncwarp(c.gm);
 }
 
 template <typename R>
 __device__ R wide_length(const WideCtx<R>& c) {
   R l = R(0);
-  for (int k = c.lane; k < c.L.S; k += 32) l += c.sm[c.L.nu + k];
-  return warp_sum(l);
+  for (int k = c.lane; k < c.L.S; k += c.lp) l += c.sm[c.L.nu + k];
+  return warp_sum(l, c.lp, c.gm);
 }
 
 template <typename R>
 __device__ R wide_dot(const WideCtx<R>& c, const R* a, const R* b) {
   R acc = R(0);
-  for (int j = c.lane; j < c.L.m; j += 32) acc = fma(a[j], b[j], acc);
-  return warp_sum(acc);
+  for (int j = c.lane; j < c.L.m; j += c.lp) acc = fma(a[j], b[j], acc);
+  return warp_sum(acc, c.lp, c.gm);
 }
 
 // out = H v (rows across lanes; each row and v read as 16-byte vectors, the
-// products accumulated in column order). A lane's rows (j, j + 32, ...) run
+// products accumulated in column order). A lane's rows (j, j + lp, ...) run
 // their chains side by side: independent FMA chains hide each other's latency.
 template <typename R, int NR>
 __device__ __forceinline__ void wide_matvec_rows(const WideCtx<R>& c, const R* v, R* out, R sign) {
@@ -180,7 +183,7 @@ __device__ __forceinline__ void wide_matvec_rows(const WideCtx<R>& c, const R* v
   R acc[NR];
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
-    const int j = c.lane + 32 * r;
+    const int j = c.lane + c.lp * r;
     h[r] = c.sm + L.H + (j < L.m ? j : 0) * L.ld;  // past the last row: row 0, result dropped
     acc[r] = R(0);
   }
@@ -201,18 +204,18 @@ __device__ __forceinline__ void wide_matvec_rows(const WideCtx<R>& c, const R* v
     for (int r = 0; r < NR; ++r) acc[r] = fma(h[r][q], v[q], acc[r]);
 #pragma unroll
   for (int r = 0; r < NR; ++r)
-    if (c.lane + 32 * r < L.m) out[c.lane + 32 * r] = sign * acc[r];
+    if (c.lane + c.lp * r < L.m) out[c.lane + c.lp * r] = sign * acc[r];
 }
 
-// NRMAX: the most rows a lane owns in this kernel instantiation (m <= 32 NRMAX).
+// NRMAX: the most rows a lane owns in this kernel instantiation (m <= lp NRMAX).
 template <typename R, int NRMAX>
 __device__ void wide_matvec(const WideCtx<R>& c, const R* v, R* out, R sign) {
-  const int nr = (c.L.m + 31) / 32;  // rows per lane, warp-uniform (no divergence)
+  const int nr = (c.L.m + c.lp - 1) / c.lp;  // rows per lane, the same on every lane of the path
   if (nr == 1) wide_matvec_rows<R, 1>(c, v, out, sign);
   if constexpr (NRMAX >= 2) if (nr == 2) wide_matvec_rows<R, 2>(c, v, out, sign);
   if constexpr (NRMAX >= 3) if (nr == 3) wide_matvec_rows<R, 3>(c, v, out, sign);
   if constexpr (NRMAX >= 4) if (nr == 4) wide_matvec_rows<R, 4>(c, v, out, sign);
-  __syncwarp();
+  __syncwarp(c.gm);
 }
 
 // The BFGS update of the rows of this lane, the reference's expression per
@@ -228,7 +231,7 @@ __device__ __forceinline__ void wide_update_rows(const WideCtx<R>& c, const R* s
   bool live[NR];
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
-    const int j0 = c.lane + 32 * r;
+    const int j0 = c.lane + c.lp * r;
     live[r] = j0 < L.m;
     const int j = live[r] ? j0 : 0;  // past the last row: row 0, computed, never stored
     h[r] = c.sm + L.H + j * L.ld;
@@ -261,7 +264,7 @@ __device__ __forceinline__ void wide_update_rows(const WideCtx<R>& c, const R* s
 
 template <typename R, int NRMAX>
 __device__ void wide_update(const WideCtx<R>& c, const R* stp, const R* hy, R rho, R coef) {
-  const int nr = (c.L.m + 31) / 32;
+  const int nr = (c.L.m + c.lp - 1) / c.lp;
   if (nr == 1) wide_update_rows<R, 1>(c, stp, hy, rho, coef);
   if constexpr (NRMAX >= 2) if (nr == 2) wide_update_rows<R, 2>(c, stp, hy, rho, coef);
   if constexpr (NRMAX >= 3) if (nr == 3) wide_update_rows<R, 3>(c, stp, hy, rho, coef);
@@ -269,9 +272,8 @@ __device__ void wide_update(const WideCtx<R>& c, const R* stp, const R* hy, R rh
 }
 
 template <typename R>
-__device__ __forceinline__ R warp_absmax(R v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = absmax_nan(v, __shfl_xor_sync(0xffffffffu, v, o));
+__device__ __forceinline__ R warp_absmax(R v, int lp, unsigned gm) {
+  for (int o = lp >> 1; o > 0; o >>= 1) v = absmax_nan(v, __shfl_xor_sync(gm, v, o));
   return v;
 }
 
@@ -281,7 +283,7 @@ __device__ R wide_step_size(const WideCtx<R>& c, const R* p, int fp_iters, bool&
   const WideLayout& L = c.L;
   R* sm = c.sm;
   R a2sum = R(0);
-  for (int k = c.lane; k < L.S; k += 32) {
+  for (int k = c.lane; k < L.S; k += c.lp) {
     R dd[3];
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
@@ -297,11 +299,11 @@ __device__ R wide_step_size(const WideCtx<R>& c, const R* p, int fp_iters, bool&
     sm[L.a2c + 2 * k + 1] = cc;
     a2sum += a2;
   }
-  zero = warp_sum(a2sum) <= Num<R>::tiny();
+  zero = warp_sum(a2sum, c.lp, c.gm) <= Num<R>::tiny();
   R alpha = R(0);
   for (int f = 0; f < fp_iters; ++f) {
     R num = R(0), den = R(0);
-    for (int k = c.lane; k < L.S; k += 32) {
+    for (int k = c.lane; k < L.S; k += c.lp) {
       const R* s = sm + L.s + 3 * k;
       const R* dd = sm + L.d + 3 * k;
       R e[3];
@@ -312,12 +314,12 @@ __device__ R wide_step_size(const WideCtx<R>& c, const R* p, int fp_iters, bool&
       num += Num<R>::div(sm[L.a2c + 2 * k + 1], n);
       den += Num<R>::div(sm[L.a2c + 2 * k], n);
     }
-    num = warp_sum(num);
-    den = warp_sum(den);
+    num = warp_sum(num, c.lp, c.gm);
+    den = warp_sum(den, c.lp, c.gm);
     const R cand = -Num<R>::div(num, zero ? R(1) : den);
     alpha = (zero || !finite(cand)) ? alpha : cand;
   }
-  __syncwarp();
+  __syncwarp(c.gm);
   return alpha;
 }
 
@@ -336,7 +338,7 @@ __device__ uint8_t wide_vjp(const WideCtx<R>& c, const PathArgs<R>& a, int64_t r
   const R* vT = has_v ? a.vT + row * 2 * K : nullptr;
   // per interaction: active flags, Hessian blocks, rhs
   R trace = R(0);
-  for (int i = c.lane; i < K; i += 32) {
+  for (int i = c.lane; i < K; i += c.lp) {
     bool act[2];
 #pragma unroll
     for (int cc = 0; cc < 2; ++cc) {
@@ -385,8 +387,8 @@ __device__ uint8_t wide_vjp(const WideCtx<R>& c, const PathArgs<R>& a, int64_t r
         }
     }
   }
-  trace = warp_sum(trace);
-  __syncwarp();
+  trace = warp_sum(trace, c.lp, c.gm);
+  __syncwarp(c.gm);
   if (need_solve) {
     if (c.lane == 0) {
       // _solve_sym (implicit_diff.py:55-71): block-Thomas elimination, accepted
@@ -504,16 +506,16 @@ __device__ uint8_t wide_vjp(const WideCtx<R>& c, const PathArgs<R>& a, int64_t r
         for (int i = 0; i < 2 * K; ++i) sm[L.sol + i] = R(0);
       sm[L.red] = solved ? R(1) : R(0);
     }
-    __syncwarp();
+    __syncwarp(c.gm);
     if (sm[L.red] == R(0)) st |= FP_STATUS_SINGULAR;
   }
   // param_vjp with the solution + wl * length partials (objective.py:89-135)
-  for (int i = c.lane; i < K; i += 32)
+  for (int i = c.lane; i < K; i += c.lp)
 #pragma unroll
     for (int r = 0; r < 3; ++r)
       sm[L.dx + 3 * i + r] = fma(c.Aij(i, r, 1), sm[L.sol + 2 * i + 1], c.Aij(i, r, 0) * sm[L.sol + 2 * i]);
-  __syncwarp();
-  for (int k = c.lane; k < L.S; k += 32) {
+  __syncwarp(c.gm);
+  for (int k = c.lane; k < L.S; k += c.lp) {
     const R* u = sm + L.u + 3 * k;
     R ds[3];
 #pragma unroll
@@ -527,9 +529,9 @@ __device__ uint8_t wide_vjp(const WideCtx<R>& c, const PathArgs<R>& a, int64_t r
 #pragma unroll
     for (int r = 0; r < 3; ++r) sm[L.w + 3 * k + r] = (ds[r] - u[r] * ud) * rk;
   }
-  __syncwarp();
+  __syncwarp(c.gm);
   bool fin = true;
-  for (int i = c.lane; i < K; i += 32) {
+  for (int i = c.lane; i < K; i += c.lp) {
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
       const R q = sm[L.u + 3 * i + r] - sm[L.u + 3 * (i + 1) + r];
@@ -557,7 +559,7 @@ __device__ uint8_t wide_vjp(const WideCtx<R>& c, const PathArgs<R>& a, int64_t r
     if (a.d_start) a.d_start[row * 3 + r] = d0;
     if (a.d_end) a.d_end[row * 3 + r] = d1;
   }
-  if (!__all_sync(0xffffffffu, fin)) st |= FP_STATUS_NONFINITE;
+  if (!__all_sync(c.gm, fin)) st |= FP_STATUS_NONFINITE;
   return st;
 }
 
@@ -571,30 +573,40 @@ __device__ uint8_t wide_vjp(const WideCtx<R>& c, const PathArgs<R>& a, int64_t r
 #ifndef FP_WIDE_MIN_BLOCKS_R2
 #define FP_WIDE_MIN_BLOCKS_R2 1
 #endif
-template <int NRMAX>
+#ifndef FP_WIDE_MIN_BLOCKS_L16
+#define FP_WIDE_MIN_BLOCKS_L16 6
+#endif
+template <int NRMAX, int LP>
 struct WideMin {
-  static constexpr int value = NRMAX == 1 ? FP_WIDE_MIN_BLOCKS_R1 : NRMAX == 2 ? FP_WIDE_MIN_BLOCKS_R2 : 1;
+  static constexpr int value = LP == 16     ? FP_WIDE_MIN_BLOCKS_L16
+                               : NRMAX == 1 ? FP_WIDE_MIN_BLOCKS_R1
+                               : NRMAX == 2 ? FP_WIDE_MIN_BLOCKS_R2
+                                            : 1;
 };
-template <typename R, int OP, int NRMAX>
-__global__ void __launch_bounds__(kWideThreads, WideMin<NRMAX>::value) wide_kernel(const __grid_constant__ PathArgs<R> a, int K,
-                                                            int wpb) {
+// LP lanes per path: 32 (one path per warp) or 16 (two paths per warp, for
+// orders whose segment and row loops leave most of a warp idle).
+template <typename R, int OP, int NRMAX, int LP>
+__global__ void __launch_bounds__(kWideThreads, (WideMin<NRMAX, LP>::value))
+    wide_kernel(const __grid_constant__ PathArgs<R> a, int K, int ppb) {
+  static_assert(LP == 16 || LP == 32, "16 or 32 lanes per path");
   extern __shared__ __align__(16) unsigned char wide_smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp >= wpb) return;
+  const int slot = int(threadIdx.x) / LP, lane = int(threadIdx.x) & (LP - 1);
+  const unsigned gm = LP == 32 ? 0xffffffffu : (0xffffu << (threadIdx.x & 16));
+  if (slot >= ppb) return;
   const WideLayout L(K, int(sizeof(R)));
-  const int64_t row = a.row_begin + int64_t(blockIdx.x) * wpb + warp;
-  if (row >= a.B) return;  // whole warp leaves together: only warp-level sync below
-  R* sm = reinterpret_cast<R*>(wide_smem) + size_t(warp) * L.total;
+  const int64_t row = a.row_begin + int64_t(blockIdx.x) * ppb + slot;
+  if (row >= a.B) return;  // the path's lanes leave together: only path-level sync below
+  R* sm = reinterpret_cast<R*>(wide_smem) + size_t(slot) * L.total;
   const int m = L.m;
   // ---- load ----------------------------------------------------------------
-  for (int e = lane; e < 6 * K; e += 32) sm[L.A + e] = a.basis[row * 6 * K + e];
-  for (int e = lane; e < 3 * K; e += 32) sm[L.b + e] = a.anchor[row * 3 * K + e];
-  for (int e = lane; e < m; e += 32) sm[L.t + e] = a.T[row * m + e];
+  for (int e = lane; e < 6 * K; e += LP) sm[L.A + e] = a.basis[row * 6 * K + e];
+  for (int e = lane; e < 3 * K; e += LP) sm[L.b + e] = a.anchor[row * 3 * K + e];
+  for (int e = lane; e < m; e += LP) sm[L.t + e] = a.T[row * m + e];
   if (lane < 3) {
     sm[L.x + lane] = a.start[row * 3 + lane];
     sm[L.x + 3 * (K + 1) + lane] = a.end[row * 3 + lane];
   }
-  __syncwarp();
+  __syncwarp(gm);
   R eps;
   {
     const double dx = double(sm[L.x + 3 * (K + 1)]) - double(sm[L.x]);
@@ -602,17 +614,17 @@ __global__ void __launch_bounds__(kWideThreads, WideMin<NRMAX>::value) wide_kern
     const double dz = double(sm[L.x + 3 * (K + 1) + 2]) - double(sm[L.x + 2]);
     eps = R(1e-12 * (1.0 + __dsqrt_rn(__fma_rn(dz, dz, __fma_rn(dy, dy, dx * dx)))));
   }
-  const WideCtx<R> c{L, sm, lane, eps};
+  const WideCtx<R> c{L, sm, lane, LP, gm, eps};
   R* t = sm + L.t;
   R* g = sm + L.g;
   wide_eval(c, t, g);
   uint8_t st = 0;
   if (OP != OP_VJP) {
     R n0 = Num<R>::inf();
-    for (int k = lane; k < L.S; k += 32) n0 = sm[L.nu + k] < n0 ? sm[L.nu + k] : n0;
-    if (warp_min(n0) <= eps) st |= FP_STATUS_DEGENERATE_ENTRY;  // checked_segments (solver.py:166)
+    for (int k = lane; k < L.S; k += LP) n0 = sm[L.nu + k] < n0 ? sm[L.nu + k] : n0;
+    if (warp_min(n0, LP, gm) <= eps) st |= FP_STATUS_DEGENERATE_ENTRY;  // checked_segments (solver.py:166)
     R* H = sm + L.H;
-    for (int j = lane; j < m; j += 32)
+    for (int j = lane; j < m; j += LP)
       for (int q = 0; q < m; ++q) H[j * L.ld + q] = j == q ? R(1) : R(0);
     R hbound = R(1);  // >= max |H_ij| (the update's overflow pre-check)
     const bool last_dead = a.H_out == nullptr && a.trace_len == nullptr;
@@ -621,27 +633,27 @@ __global__ void __launch_bounds__(kWideThreads, WideMin<NRMAX>::value) wide_kern
     R* gn = sm + L.gn;
     R* y = sm + L.y;
     R* hy = sm + L.hy;
-    __syncwarp();
+    __syncwarp(gm);
     for (int it = 0; it < a.iterations; ++it) {
       wide_matvec<R, NRMAX>(c, g, p, R(-1));  // p = -H g
       bool zero;
       const R alpha = wide_step_size(c, p, a.fp_iters, zero);
       if (zero) st |= FP_STATUS_ZERO_DIRECTION;
       uint8_t fate = zero ? FP_FATE_ZERO_DIRECTION : 0;
-      for (int j = lane; j < m; j += 32) {
+      for (int j = lane; j < m; j += LP) {
         stp[j] = alpha * p[j];
         t[j] = t[j] + stp[j];
       }
-      __syncwarp();
+      __syncwarp(gm);
       wide_eval(c, t, gn);
       if (last_dead && it == a.iterations - 1) {
         // the last update and its curvature test feed nothing read afterwards
-        for (int j = lane; j < m; j += 32) g[j] = gn[j];
-        __syncwarp();
+        for (int j = lane; j < m; j += LP) g[j] = gn[j];
+        __syncwarp(gm);
         break;
       }
-      for (int j = lane; j < m; j += 32) y[j] = gn[j] - g[j];
-      __syncwarp();
+      for (int j = lane; j < m; j += LP) y[j] = gn[j] - g[j];
+      __syncwarp(gm);
       const R sy = wide_dot(c, stp, y);
       const R sn = Num<R>::sqrt_(wide_dot(c, stp, stp));
       const R yn = Num<R>::sqrt_(wide_dot(c, y, y));
@@ -660,12 +672,12 @@ __global__ void __launch_bounds__(kWideThreads, WideMin<NRMAX>::value) wide_kern
         // above it (or on a NaN, which the NaN-propagating maxima carry).
         // Same verdicts as checking every entry.
         R ms = R(0), mh = R(0);
-        for (int j = lane; j < m; j += 32) {
+        for (int j = lane; j < m; j += LP) {
           ms = absmax_nan(ms, stp[j]);
           mh = absmax_nan(mh, hy[j]);
         }
-        ms = warp_absmax(ms);
-        mh = warp_absmax(mh);
+        ms = warp_absmax(ms, LP, gm);
+        mh = warp_absmax(mh, LP, gm);
         const R am = ms * mh, ss = ms * ms;
         const R r2a = R(2) * fabs(rho) * am, cs = fabs(coef) * ss;
         const R nb = (hbound + r2a) + cs;
@@ -674,7 +686,7 @@ __global__ void __launch_bounds__(kWideThreads, WideMin<NRMAX>::value) wide_kern
         R mx = R(0);
         const bool checked = !(big < Num<R>::suspect());
         if (checked) {
-          for (int j = lane; j < m; j += 32) {
+          for (int j = lane; j < m; j += LP) {
             const R* h = H + j * L.ld;
             for (int q = 0; q < m; ++q) {
               const R v = (h[q] - rho * (stp[j] * hy[q] + stp[q] * hy[j])) + coef * (stp[j] * stp[q]);
@@ -682,8 +694,8 @@ __global__ void __launch_bounds__(kWideThreads, WideMin<NRMAX>::value) wide_kern
               mx = fabs(v) > mx ? fabs(v) : mx;
             }
           }
-          fin = __all_sync(0xffffffffu, fin);
-          mx = warp_absmax(mx);
+          fin = __all_sync(gm, fin);
+          mx = warp_absmax(mx, LP, gm);
         }
         if (checked) fate |= FP_FATE_ENTRY_CHECK;
         if (!fin) fate |= FP_FATE_NONFINITE_SKIP;
@@ -691,10 +703,10 @@ __global__ void __launch_bounds__(kWideThreads, WideMin<NRMAX>::value) wide_kern
           wide_update<R, NRMAX>(c, stp, hy, rho, coef);
           hbound = checked ? mx * R(1.0009765625) : nb;
         }
-        __syncwarp();
+        __syncwarp(gm);
       }
-      for (int j = lane; j < m; j += 32) g[j] = gn[j];
-      __syncwarp();
+      for (int j = lane; j < m; j += LP) g[j] = gn[j];
+      __syncwarp(gm);
       if (a.trace_len != nullptr) {
         const R len = wide_length(c);
         const R gq = wide_dot(c, g, g);
@@ -706,28 +718,28 @@ __global__ void __launch_bounds__(kWideThreads, WideMin<NRMAX>::value) wide_kern
       }
     }
     if (a.H_out != nullptr)
-      for (int j = lane; j < m; j += 32)
+      for (int j = lane; j < m; j += LP)
         for (int q = 0; q < m; ++q) a.H_out[(row * m + j) * m + q] = H[j * L.ld + q];
   }
   // ---- final classification (as final_status) ------------------------------------
   const R len = wide_length(c);
   R nmin = Num<R>::inf();
-  for (int k = lane; k < L.S; k += 32) nmin = sm[L.nu + k] < nmin ? sm[L.nu + k] : nmin;
-  nmin = warp_min(nmin);
+  for (int k = lane; k < L.S; k += LP) nmin = sm[L.nu + k] < nmin ? sm[L.nu + k] : nmin;
+  nmin = warp_min(nmin, LP, gm);
   const R gq = wide_dot(c, g, g);
   if (!(Num<R>::sqrt_(gq) < R(1e-5) * (R(1) + len))) st |= FP_STATUS_NOT_STATIONARY;
   if (nmin <= eps) st |= FP_STATUS_DEGENERATE_FINAL;
   if (nmin < R(1e-3)) st |= FP_STATUS_SHORT_SEGMENT;
   bool fin = finite(len);
-  for (int j = lane; j < m; j += 32) fin = fin && finite(t[j]) && finite(g[j]);
-  if (!__all_sync(0xffffffffu, fin)) st |= FP_STATUS_NONFINITE;
+  for (int j = lane; j < m; j += LP) fin = fin && finite(t[j]) && finite(g[j]);
+  if (!__all_sync(gm, fin)) st |= FP_STATUS_NONFINITE;
   if (OP != OP_VJP) {
-    for (int j = lane; j < m; j += 32) {
+    for (int j = lane; j < m; j += LP) {
       if (a.T_out) a.T_out[row * m + j] = t[j];
       if (a.g_out) a.g_out[row * m + j] = g[j];
     }
     if (a.points_out)
-      for (int e = lane; e < 3 * K; e += 32) a.points_out[row * 3 * K + e] = sm[L.x + 3 + e];
+      for (int e = lane; e < 3 * K; e += LP) a.points_out[row * 3 * K + e] = sm[L.x + 3 + e];
     if (a.length_out && lane == 0) a.length_out[row] = len;
   }
   if (OP != OP_SOLVE) st |= wide_vjp(c, a, row, t);
@@ -738,9 +750,22 @@ __global__ void __launch_bounds__(kWideThreads, WideMin<NRMAX>::value) wide_kern
 
 size_t wide_smem_per_path(int K, size_t elem) { return size_t(WideLayout(K, int(elem)).total) * elem; }
 
-template <typename R, int NRMAX>
-cudaError_t launch_wide(int op, const PathArgs<R>& a, int K, int wpb, int64_t blocks, int threads,
+template <typename R, int NRMAX, int LP>
+cudaError_t launch_wide(int op, const PathArgs<R>& a, int K, int ppb, int64_t blocks, int threads,
                         size_t smem, cudaStream_t s);
+
+// Orders up to FP_WIDE_LP16_MAX_K_F32 / _F64 run two paths per warp (16 lanes
+// each); 0 keeps one path per warp (A/B builds). Measured (profiles/
+// r02x_ab_wide_lp16.txt, fused step, 20 iterations): fp32 K=9 4.77 -> 3.02
+// ms, K=12 3.69 -> 2.47, K=15 3.39 -> 3.03, K=16 2.90 -> 3.03; fp64 K=9 6.31
+// -> 5.76, K=11 5.54 -> 4.96, K=12 5.19 -> 6.42 (shared memory per path
+// doubles, fewer CTAs fit).
+#ifndef FP_WIDE_LP16_MAX_K_F32
+#define FP_WIDE_LP16_MAX_K_F32 15
+#endif
+#ifndef FP_WIDE_LP16_MAX_K_F64
+#define FP_WIDE_LP16_MAX_K_F64 11
+#endif
 
 template <typename R>
 cudaError_t dispatch_wide(int K, const PathArgs<R>& a, int op, cudaStream_t s) {
@@ -751,40 +776,44 @@ cudaError_t dispatch_wide(int K, const PathArgs<R>& a, int op, cudaStream_t s) {
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  int wpb = int(size_t(optin) / per);
-  wpb = wpb > kWideThreads / 32 ? kWideThreads / 32 : wpb;
-  if (wpb < 1) return cudaErrorInvalidValue;
-  const size_t smem = per * size_t(wpb);
-  const int64_t blocks = (rows + wpb - 1) / wpb;
-  const int threads = 32 * wpb;
-  const int nrmax = (2 * K + 31) / 32;
+  const int lp = K <= (sizeof(R) == 4 ? FP_WIDE_LP16_MAX_K_F32 : FP_WIDE_LP16_MAX_K_F64) ? 16 : 32;
+  int ppb = int(size_t(optin) / per);  // paths per CTA
+  ppb = ppb > kWideThreads / lp ? kWideThreads / lp : ppb;
+  if (ppb < 1) return cudaErrorInvalidValue;
+  const size_t smem = per * size_t(ppb);
+  const int64_t blocks = (rows + ppb - 1) / ppb;
+  const int threads = (ppb * lp + 31) / 32 * 32;
+  const int nrmax = (2 * K + lp - 1) / lp;
+  if (lp == 16) return launch_wide<R, 2, 16>(op, a, K, ppb, blocks, threads, smem, s);
   switch (nrmax) {
-    case 1: return launch_wide<R, 1>(op, a, K, wpb, blocks, threads, smem, s);
-    case 2: return launch_wide<R, 2>(op, a, K, wpb, blocks, threads, smem, s);
-    default: return launch_wide<R, 4>(op, a, K, wpb, blocks, threads, smem, s);
+    case 1: return launch_wide<R, 1, 32>(op, a, K, ppb, blocks, threads, smem, s);
+    case 2: return launch_wide<R, 2, 32>(op, a, K, ppb, blocks, threads, smem, s);
+    default: return launch_wide<R, 4, 32>(op, a, K, ppb, blocks, threads, smem, s);
   }
 }
 
-template <typename R, int NRMAX>
-cudaError_t launch_wide(int op, const PathArgs<R>& a, int K, int wpb, int64_t blocks, int threads,
+template <typename R, int NRMAX, int LP>
+cudaError_t launch_wide(int op, const PathArgs<R>& a, int K, int ppb, int64_t blocks, int threads,
                         size_t smem, cudaStream_t s) {
   cudaError_t e;
   switch (op) {
     case OP_SOLVE:
-      e = cudaFuncSetAttribute(wide_kernel<R, OP_SOLVE, NRMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(smem));
-      if (e == cudaSuccess) wide_kernel<R, OP_SOLVE, NRMAX><<<unsigned(blocks), threads, smem, s>>>(a, K, wpb);
-      break;
-    case OP_SOLVE_VJP:
-      e = cudaFuncSetAttribute(wide_kernel<R, OP_SOLVE_VJP, NRMAX>,
+      e = cudaFuncSetAttribute(wide_kernel<R, OP_SOLVE, NRMAX, LP>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       if (e == cudaSuccess)
-        wide_kernel<R, OP_SOLVE_VJP, NRMAX><<<unsigned(blocks), threads, smem, s>>>(a, K, wpb);
+        wide_kernel<R, OP_SOLVE, NRMAX, LP><<<unsigned(blocks), threads, smem, s>>>(a, K, ppb);
+      break;
+    case OP_SOLVE_VJP:
+      e = cudaFuncSetAttribute(wide_kernel<R, OP_SOLVE_VJP, NRMAX, LP>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      if (e == cudaSuccess)
+        wide_kernel<R, OP_SOLVE_VJP, NRMAX, LP><<<unsigned(blocks), threads, smem, s>>>(a, K, ppb);
       break;
     case OP_VJP:
-      e = cudaFuncSetAttribute(wide_kernel<R, OP_VJP, NRMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(smem));
-      if (e == cudaSuccess) wide_kernel<R, OP_VJP, NRMAX><<<unsigned(blocks), threads, smem, s>>>(a, K, wpb);
+      e = cudaFuncSetAttribute(wide_kernel<R, OP_VJP, NRMAX, LP>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      if (e == cudaSuccess)
+        wide_kernel<R, OP_VJP, NRMAX, LP><<<unsigned(blocks), threads, smem, s>>>(a, K, ppb);
       break;
     default:
       return cudaErrorInvalidValue;

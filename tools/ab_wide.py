@@ -1,6 +1,6 @@
 """Bitwise comparison and timing of two libraries on the long-path solver (orders 9..64).
 
-    python tools/ab_wide.py libA.so libB.so [iterations]
+    python tools/ab_wide.py libA.so libB.so [iterations] [orders, e.g. 9,12,16]
 
 Both libraries are loaded side by side with ctypes; the same device inputs
 (the tools/wide_rate.py batches: 2^20 / K paths of one mixed ordering) go
@@ -30,8 +30,9 @@ def load(path):
 
 libs = [load(sys.argv[1]), load(sys.argv[2])]
 iters = int(sys.argv[3]) if len(sys.argv) > 3 else 20
+orders = [int(k) for k in sys.argv[4].split(",")] if len(sys.argv) > 4 else [9, 16, 33, 64]
 dev = torch.device("cuda")
-for K in (9, 16, 33, 64):
+for K in orders:
     n = (1 << 20) // K
     order = "".join("RD"[(i * 7 + K) % 3 == 0] for i in range(K))
     b = datagen.gen_batch(200 + K, [order], n)
