@@ -91,6 +91,32 @@ def test_wide_fused_equals_solve_then_vjp():
         assert torch.equal(torch.nan_to_num(a, 7.0), torch.nan_to_num(b, 7.0))
 
 
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_two_paths_per_warp_are_independent(prec):
+    """Orders up to 15 (fp32) / 11 (fp64) run two paths per warp, 16 lanes
+    each (csrc/fp_wide.cu), with every shuffle, vote and barrier masked to the
+    path's half. Neighbouring paths that take different branches (a NaN row
+    whose updates are all skipped next to healthy rows, all-edge next to
+    mixed orderings) still get exactly the bits each gets alone — in a batch
+    of one, where the other half-warp has no path and leaves at once."""
+    from paper_2510_16172_b200 import datagen
+
+    b = datagen.gen_batch(31, ["RDRRDRDDR", "DDDDDDDDD"], 6)
+    basis, anchor, start, end, T0 = (np.array(x) for x in (b.basis, b.anchor, b.start, b.end, b.T0))
+    anchor[3, 2, 0] = np.nan
+    opts = SolveOptions(iterations=30, precision=Precision.SINGLE if prec == "f32" else Precision.DOUBLE)
+    res, grads = solve_with_gradients(BatchScene(basis, anchor, start, end), T0, opts)
+    torch.cuda.synchronize()
+    assert int(res.status[3]) & 0x08  # the NaN row is flagged non-finite
+    for i in range(b.size):
+        r1, g1 = solve_with_gradients(BatchScene(basis[i:i + 1], anchor[i:i + 1], start[i:i + 1], end[i:i + 1]),
+                                      T0[i:i + 1], opts)
+        for x, y in ((res.T[i:i + 1], r1.T), (res.length[i:i + 1], r1.length), (res.status[i:i + 1], r1.status),
+                     (grads.basis[i:i + 1], g1.basis), (grads.anchor[i:i + 1], g1.anchor),
+                     (grads.start[i:i + 1], g1.start), (grads.end[i:i + 1], g1.end)):
+            assert torch.equal(torch.nan_to_num(x.double(), 7.0), torch.nan_to_num(y.double(), 7.0)), i
+
+
 def test_order_above_64_rejected():
     from paper_2510_16172_b200 import datagen
 
