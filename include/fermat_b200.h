@@ -45,7 +45,8 @@ enum fp_error {
 
 /* Largest interaction count: the reference's MAX_INTERACTIONS (geometry.py:23).
  * Orders 1..8 run the register-resident per-thread kernels, orders 9..64 the
- * warp-per-path solver (csrc/fp_wide.cu); larger K is FP_ERR_UNSUPPORTED_ORDER. */
+ * warp-per-path solver (csrc/fp_wide.cu; two paths per warp up to order 15 in
+ * fp32, 11 in fp64); larger K is FP_ERR_UNSUPPORTED_ORDER. */
 #define FP_MAX_ORDER 64
 
 /* ---- per-path status bits (uint8) --------------------------------------- */
