@@ -282,6 +282,46 @@ def measure_ffma_peak(lib, stream, dev, register_operands=False):
     return best
 
 
+def pcie_link(h2d: int, d2h: int, dev, e2e_s: float, reps: int = 3) -> dict:
+    """The end-to-end step's bound: the same byte counts moved between pinned
+    host memory and the device by plain copies, each direction alone and both
+    at once on two streams (copy engines only, no kernel). `frac` = that
+    duplex copy time / the e2e step time."""
+    import torch
+
+    hi = torch.empty(h2d, dtype=torch.uint8, pin_memory=True)
+    ho = torch.empty(d2h, dtype=torch.uint8, pin_memory=True)
+    di = torch.empty(h2d, dtype=torch.uint8, device=dev)
+    do = torch.empty(d2h, dtype=torch.uint8, device=dev)
+    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def timed(parts):
+        best = float("inf")
+        for _ in range(reps):
+            torch.cuda.synchronize(dev)
+            evs = []
+            for st, fn in parts:
+                with torch.cuda.stream(st):
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record(st)
+                    fn()
+                    b.record(st)
+                    evs.append((a, b))
+            torch.cuda.synchronize(dev)
+            # concurrent parts start together: the span is max(end) - min(start)
+            t = max(max(a.elapsed_time(b2) for b2 in (b for _, b in evs)) for a, _ in evs)
+            best = min(best, t)
+        return best
+
+    cin = (s_in, lambda: di.copy_(hi, non_blocking=True))
+    cout = (s_out, lambda: ho.copy_(do, non_blocking=True))
+    t_in, t_out, t_both = timed([cin]), timed([cout]), timed([cin, cout])
+    return {"h2d_gbs": h2d / t_in / 1e6, "d2h_gbs": d2h / t_out / 1e6, "h2d_ms": t_in, "d2h_ms": t_out,
+            "duplex_ms": t_both, "frac": t_both / (e2e_s * 1e3),
+            "what": "pinned host <-> device copies of the step's h2d / d2h bytes, alone and concurrent "
+                    "(two streams, best of 3); frac = duplex_ms / e2e ms_per_step"}
+
+
 def cpu_sample(batch, n: int):
     """A bounded, ordering-balanced sample of the workload (every ordering equally)."""
     K = batch.order
@@ -551,7 +591,8 @@ def run_ours(args):
                "blocking": {"ms_per_step": e_blocking_s * 1e3,
                             "value": _sum_over_ranks(e_conv, ws, dev) / e_blocking_s,
                             "path": ("fp_solve_vjp_host_f32 (one blocking call per step; chunks of "
-                                     f"{args.chunk} paths over 3 slots)")}}
+                                     f"{args.chunk} paths over 3 slots)")},
+               "link": pcie_link(h2d, d2h, dev, e_s)}
 
     # ---- CPU baseline (rank 0, N=1 only) ----------------------------------------------
     cpu = None
