@@ -684,7 +684,8 @@ __device__ __forceinline__ void bfgs_iterations(const Geo<R, K>& G, PathState<R,
     P.template eval<true>(G, gn);
   };
   // Short loop bodies (order 1) run two iterations per trip: -1.2% at K=1
-  // (tools/ab_libs.sh; at K=3 unrolling measured slower, instruction cache).
+  // (tools/ab_libs.sh; at K=3 unrolling measured slower, instruction cache;
+  // at K=2 fused 0.704 -> 0.7125 ms, profiles/r02z_ab_unroll2.txt).
   constexpr int kUnroll = (K <= kUnrollMaxOrder && !GENERAL) ? 2 : 1;
 #pragma unroll(kUnroll)
   for (int it = 0; it < n_loop; ++it) {
