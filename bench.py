@@ -540,18 +540,23 @@ def run_ours(args):
             if rc:
                 _lib.check(rc, "fp_solve_vjp_host_f32")
 
-        # Streaming through the public submit / wait API: step i + 1 is
-        # submitted before step i is waited for, so its host-to-device copies
-        # overlap step i's device-to-host copies (two output sets in flight).
-        # Every step still copies its inputs in and its results out.
-        hout2 = [hout, [None if t is None else pin(tuple(t.shape), t.dtype) for t in hout]]
+        # Streaming through the public submit / wait API: step i is waited
+        # for only after step i + lag was submitted, so later steps' host-to-
+        # device copies and kernels are already queued while step i's results
+        # stream out (lag + 1 output sets in flight). Every step still copies
+        # its inputs in and its results out.
+        lag = max(1, args.e2e_lag)
+        hout2 = [hout] + [[None if t is None else pin(tuple(t.shape), t.dtype) for t in hout]
+                          for _ in range(lag)]
+        nsets = len(hout2)
         import ctypes
 
         def e2e_submit(i):
             tk = ctypes.c_uint64(0)
             rc = lib.fp_solve_vjp_host_submit_f32(*(P(t) for t in hin), None, B, K, I, F, 1.0,
-                                                  _lib.VJP_FULL, *(Pn(t) for t in hout2[i % 2]),
-                                                  args.stream_chunk, 2, ctypes.addressof(tk))
+                                                  _lib.VJP_FULL, *(Pn(t) for t in hout2[i % nsets]),
+                                                  args.stream_chunk, args.stream_slots,
+                                                  ctypes.addressof(tk))
             if rc:
                 _lib.check(rc, "fp_solve_vjp_host_submit_f32")
             return tk.value
@@ -569,21 +574,21 @@ def run_ours(args):
         e2e_wait(e2e_submit(0))
         _barrier(ws)
         t0 = time.perf_counter()
-        prev = None
+        pending = []
         for i in range(e_steps):
-            tk = e2e_submit(i)
-            if prev is not None:
-                e2e_wait(prev)
-            prev = tk
-        e2e_wait(prev)
+            pending.append(e2e_submit(i))
+            if len(pending) > lag:
+                e2e_wait(pending.pop(0))
+        for tk in pending:
+            e2e_wait(tk)
         e_s = _max_over_ranks((time.perf_counter() - t0) / e_steps, ws, dev)
-        e_conv = int(((hout2[(e_steps - 1) % 2][7] & _lib.STATUS_UNCONVERGED_MASK) == 0).sum().item())
+        e_conv = int(((hout2[(e_steps - 1) % nsets][7] & _lib.STATUS_UNCONVERGED_MASK) == 0).sum().item())
         e2e = {"value": _sum_over_ranks(e_conv, ws, dev) / e_s, "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": e_s * 1e3, "raw_paths_per_s": paths_all / e_s,
                "path": ("fp_solve_vjp_host_submit_f32 + fp_host_wait (pinned host buffers; steps "
-                        "submitted back to back, each waited one step later; copy-in, compute and "
-                        f"copy-out streams over 2 device chunk slots of up to {args.stream_chunk} "
+                        f"submitted back to back, each waited {lag} step(s) later; copy-in, compute and "
+                        f"copy-out streams over {args.stream_slots} device chunk slots of up to {args.stream_chunk} "
                         "paths)"),
                "copies": ("in: basis, anchor, start, end (T0 = NULL: zero init on the device); "
                           "out: T, length, d_basis, d_anchor, d_start, d_end, status (points "
@@ -850,6 +855,9 @@ def main(argv=None):
     ap.add_argument("--chunk", type=int, default=1 << 19, help="e2e blocking call: pipeline chunk (paths)")
     ap.add_argument("--stream-chunk", type=int, default=1 << 22,
                     help="e2e submitted steps: pipeline chunk (paths; tools/e2e_pipe_sweep.py)")
+    ap.add_argument("--stream-slots", type=int, default=2, help="e2e submitted steps: device chunk slots")
+    ap.add_argument("--e2e-lag", type=int, default=1,
+                    help="e2e submitted steps: step i is waited for after step i + lag was submitted")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="tiny CPU samples (debugging)")
